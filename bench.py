@@ -1,0 +1,433 @@
+#!/usr/bin/env python
+"""Bench of the B200 visual-preprocessing hot path (EasyVideoR1, arXiv 2604.16893).
+
+Metric (BASELINE.json): visual tokens/s (t*h*w/m^2) and achieved HBM GB/s vs peak.
+Workload (N=1 default): cfg5 -- the GRPO rollout batch of 512 clips shaped like cfg2 (30 fps
+1280x720 source, 2 fps, <=64 frames, 262,144 px/frame -> 384x672, grid (32,24,42), 8,064 tokens
+each), sharded by clip over the ranks (strong scaling: the job is always 512 clips).
+
+One step = the whole hot path for the rank's clips, all on the device:
+  K1 vp_plan_frames -> K3 vp_resize_normalize_patchify -> K4 vp_rope_index
+  (+ N>1: vp_plan_records -> NCCL all_gather (torch.distributed) -> vp_pack_offsets).
+Inputs are synthetic u8 frames written into HBM by vp_synth_frames before timing (90.6 GB at N=1,
+larger than L2, so no L2 flush is needed).  `e2e` times the same path from pinned HOST frames,
+the host->device copies inside the timed region, pipelined clip-chunk by clip-chunk.
+
+  python bench.py [--gpus N] [--steps K] [--warmup W] [--impl ours|reference] [--clips C]
+"""
+from __future__ import annotations
+
+import argparse
+import json
+import os
+import statistics
+import subprocess
+import sys
+import tempfile
+import time
+
+import numpy as np
+
+ROOT = os.path.dirname(os.path.abspath(__file__))
+sys.path.insert(0, ROOT)
+
+METRIC = "visual tokens/sec and achieved HBM GB/s vs peak at 1/2/4/8 B200"
+UNIT = "visual tokens/s"
+JOB_CLIPS = 512
+CLOCK_FIELDS = ("index,clocks.sm,clocks.max.sm,power.draw,clocks_event_reasons.active,"
+                "clocks_event_reasons.hw_slowdown,clocks_event_reasons.hw_thermal_slowdown,"
+                "clocks_event_reasons.sw_thermal_slowdown,clocks_event_reasons.sw_power_cap")
+
+
+def cfg5_clip():
+    import vp_inputs as I
+    return I.clip(1800, 30.0, 720, 1280)
+
+
+def cfg5_params():
+    import vp_inputs as I
+    return I.qwen3_params(max_frames=64)
+
+
+def peaks():
+    try:
+        with open(os.path.join(ROOT, "MEASURED_PEAKS.json")) as f:
+            d = json.load(f)
+        return float(d["hbm_gbs"]), "measured (MEASURED_PEAKS.json hbm_gbs)"
+    except Exception:
+        return 6650.0, "fallback (B200_PROFILING.md 6.65 TB/s)"
+
+
+class ClockSampler:
+    """nvidia-smi clocks + throttle reasons sampled during the timed region."""
+
+    def __init__(self, gpu_index: int):
+        self.f = tempfile.NamedTemporaryFile("w+", suffix=".csv", delete=False)
+        try:
+            self.p = subprocess.Popen(["nvidia-smi", f"--id={gpu_index}", f"--query-gpu={CLOCK_FIELDS}",
+                                       "--format=csv,noheader,nounits", "-lms", "100"], stdout=self.f,
+                                      stderr=subprocess.DEVNULL)
+        except Exception:
+            self.p = None
+
+    def stop(self):
+        if self.p is None:
+            return None
+        self.p.terminate()
+        try:
+            self.p.wait(timeout=5)
+        except Exception:
+            self.p.kill()
+        self.f.flush()
+        rows = []
+        with open(self.f.name) as g:
+            for line in g:
+                parts = [x.strip() for x in line.split(",")]
+                if len(parts) >= 9:
+                    rows.append(parts)
+        os.unlink(self.f.name)
+        if not rows:
+            return None
+        sm = [float(r[1]) for r in rows if r[1].replace(".", "").isdigit()]
+        mx = [float(r[2]) for r in rows if r[2].replace(".", "").isdigit()]
+        names = ["hw_slowdown", "hw_thermal_slowdown", "sw_thermal_slowdown", "sw_power_cap"]
+        reasons = sorted({n for r in rows for n, v in zip(names, r[5:9]) if v.lower().startswith("active")})
+        return {"sm_mhz": statistics.median(sm) if sm else None, "sm_max_mhz": max(mx) if mx else None,
+                "reasons": reasons, "samples": len(rows)}
+
+
+# ----------------------------------------------------------------------------------------------
+# our arm
+# ----------------------------------------------------------------------------------------------
+
+def run_ours(args, rank, world, local_rank):
+    import torch
+    import torch.distributed as dist
+    import paper_2604_16893_b200 as vp
+    import vp_inputs as I
+
+    torch.cuda.set_device(local_rank)
+    dev = torch.device("cuda", local_rank)
+    job_clips = args.clips if args.clips else JOB_CLIPS
+    assert job_clips % world == 0, "clips must divide evenly over ranks"
+    per = job_clips // world
+    params = cfg5_params()
+    clips = [cfg5_clip()] * per
+    pre = vp.VisualPreprocessor(device=dev, **params)
+    P = pre.params
+    m = P.merge_size
+
+    # ---------------- setup (untimed) ----------------
+    pl = pre.plan(clips)
+    ph = pl.plans_host
+    off, pitch, total_bytes = pre.frames_layout(pl)
+    frames = torch.empty(total_bytes, dtype=torch.uint8, device=dev)
+    idx_host = pl.frame_indices.cpu().numpy()
+    for k in range(per):
+        n, H, W = int(ph["n_frames"][k]), int(ph["in_h"][k]), int(ph["in_w"][k])
+        ids = torch.from_numpy(idx_host[ph["index_offset"][k]: ph["index_offset"][k] + n].copy()).to(dev)
+        vp.synth_frames(vp.VP_SYNTH_NOISE, 1000003 * 0 + rank * per + k, ids, H, W, frames[off[k]:], int(pitch[k]))
+    off_d = torch.from_numpy(off).to(dev)
+    pitch_d = torch.from_numpy(pitch).to(dev)
+    out = pre.alloc_outputs(pl)
+    # token-type sequences: one sequence per clip (Qwen3-VL: "<t s><vision_start> group <vision_end>" per group)
+    seqs = []
+    for k in range(per):
+        gt, gh, gw = int(ph["grid_t"][k]), int(ph["grid_h"][k]), int(ph["grid_w"][k])
+        runs = [(0, 64)]
+        for _ in range(gt):
+            runs += [(0, 7), (2, gh * gw // (m * m)), (0, 1)]
+        runs.append((0, 32))
+        seqs.append(I.token_types(runs))
+    tt = torch.from_numpy(np.concatenate(seqs)).to(dev)
+    cu = torch.tensor(np.concatenate([[0], np.cumsum([len(s) for s in seqs])]), dtype=torch.int64, device=dev)
+    L = tt.numel()
+    pos = torch.empty(3, L, dtype=torch.int64, device=dev)
+    deltas = torch.empty(per, dtype=torch.int64, device=dev)
+    rst = torch.empty(per + 1, dtype=torch.int32, device=dev)
+    ws = torch.empty(vp.rope_index_workspace_bytes(per, per), dtype=torch.uint8, device=dev)
+    records = torch.empty(per * 4, dtype=torch.int32, device=dev)
+    gathered = torch.empty(world * per * 4, dtype=torch.int32, device=dev)
+    tok_off = torch.empty(world * per + 1, dtype=torch.int64, device=dev)
+    pat_off = torch.empty(world * per + 1, dtype=torch.int64, device=dev)
+    stream = torch.cuda.current_stream(dev)
+
+    tokens_rank = int(pl.totals["vid_tokens"] + pl.totals["img_tokens"])
+    in_bytes = int(sum(int(ph["n_frames"][k]) * int(ph["in_h"][k]) * 3 * int(ph["in_w"][k]) for k in range(per)))
+    out_bytes = int((pl.totals["vid_rows"] + pl.totals["img_rows"]) * pre.D * (4 if P.out_dtype else 2))
+    k3_bytes = in_bytes + out_bytes
+
+    ev_k3 = []
+
+    def step(record=False):
+        vp.plan_frames(P, pl.clips_dev, per, pl.plans_dev, pl.frame_indices, pl.totals_dev, pl.group_timestamps)
+        if world > 1:
+            vp.plan_records(pl.plans_dev, per, m, records)
+            dist.all_gather_into_tensor(gathered, records)
+            vp.pack_offsets(gathered, world, per, tok_off, pat_off)
+        if record:
+            a = torch.cuda.Event(enable_timing=True)
+            b = torch.cuda.Event(enable_timing=True)
+            a.record(stream)
+        vp.resize_normalize_patchify(P, pl.plans_dev, per, frames, off_d, pitch_d, None,
+                                     out["pixel_values_videos"], out["image_grid_thw"], out["video_grid_thw"],
+                                     out["clip_status"])
+        if record:
+            b.record(stream)
+            ev_k3.append((a, b))
+        vp.rope_index(P, vp.VP_ROPE_QWEN3_SPLIT, tt, cu, None, out["video_grid_thw"], pos, deltas, rst, ws)
+
+    launches_per_step = 5 + (2 if world > 1 else 0)
+    for _ in range(args.warmup):
+        step()
+    torch.cuda.synchronize()
+    st = out["clip_status"][:per].cpu().numpy()
+    assert (st == 0).all(), f"clip status {np.unique(st)}"
+    rs = rst.cpu().numpy()
+    assert (rs == 0).all(), "rope status mismatch"
+    if world > 1:
+        dist.barrier()
+    torch.cuda.synchronize()
+    clocks = ClockSampler(local_rank) if rank == 0 else None
+    t0 = torch.cuda.Event(enable_timing=True)
+    t1 = torch.cuda.Event(enable_timing=True)
+    t0.record(stream)
+    for _ in range(args.steps):
+        step(record=True)
+    t1.record(stream)
+    torch.cuda.synchronize()
+    if world > 1:
+        dist.barrier()
+    clk = clocks.stop() if clocks else None
+    ms_total = t0.elapsed_time(t1)
+    k3_ms = float(np.mean([a.elapsed_time(b) for a, b in ev_k3]))
+    ms_step = ms_total / args.steps
+    t = torch.tensor([ms_step, k3_ms], dtype=torch.float64, device=dev)
+    if world > 1:
+        dist.all_reduce(t, op=dist.ReduceOp.MAX)
+    ms_step, k3_ms = t.tolist()
+
+    # ---------------- e2e: pinned host frames -> device inside the timed region ----------------
+    e2e = None
+    if not args.no_e2e:
+        e2e = run_e2e(args, pre, pl, frames, off, pitch, out, tt, cu, pos, deltas, rst, ws, per, dev, world,
+                      tokens_rank)
+
+    result = None
+    if rank == 0:
+        peak, peak_src = peaks()
+        achieved = k3_bytes / (k3_ms * 1e-3) / 1e9
+        tokens_job = tokens_rank * world
+        traffic = load_traffic(per)
+        result = {
+            "metric": METRIC, "value": tokens_job / (ms_step * 1e-3), "unit": UNIT, "n_gpus": world,
+            "steps": args.steps, "warmup": args.warmup, "ms_per_step": ms_step, "higher_is_better": True,
+            "scaling": "strong", "vs_baseline": None, "dtype": "f32", "data": "synthetic",
+            "config": {"workload": f"cfg5: GRPO rollout batch of {job_clips} clips (cfg2-shaped: 30 fps 1280x720, "
+                                   f"2 fps, <=64 frames, 262144 px/frame -> 384x672, grid (32,24,42)) sharded by "
+                                   f"clip over {world} rank(s)",
+                       "clips_per_rank": per, "tokens_per_step": tokens_job,
+                       "out_dtype": "bf16" if P.out_dtype == 0 else "f32", "model_preset": "Qwen3-VL p16 m2 tp2",
+                       "l2": "inputs (%.1f GB/rank) larger than L2, no flush" % (in_bytes / 1e9),
+                       "parallelism": f"clip-sharded dp{world}"},
+            "hbm_gbs_step": k3_bytes / (ms_step * 1e-3) / 1e9,
+            "roofline": {"bound": "hbm", "achieved": achieved, "peak": peak, "unit": "GB/s",
+                         "frac": achieved / peak, "traffic": traffic, "kernel": "resize_generic_kernel (K3)",
+                         "k3_ms": k3_ms, "algorithmic_bytes_per_launch": k3_bytes, "peak_source": peak_src},
+            "gpu_launches": launches_per_step * args.steps,
+            "clocks": clk,
+            "e2e": e2e,
+        }
+    return result
+
+
+def load_traffic(clips_per_rank):
+    """ncu dram bytes per clip for K3 (profiles/traffic.json, written from an `ncu --set full` capture)."""
+    try:
+        with open(os.path.join(ROOT, "profiles", "traffic.json")) as f:
+            d = json.load(f)
+        return d["k3_dram_bytes_per_clip"] * clips_per_rank
+    except Exception:
+        return None
+
+
+def run_e2e(args, pre, pl, frames, off, pitch, out, tt, cu, pos, deltas, rst, ws, per, dev, world, tokens_rank):
+    """Same step through the public API from pinned host memory: per chunk of clips, H2D on a copy stream,
+    the resize kernel on the compute stream once the chunk has landed; then MRoPE; then D2H of the
+    grids, statuses and deltas the trainer reads.  The pinned source is a ring of `ring` clips."""
+    import torch
+    import torch.distributed as dist
+    import paper_2604_16893_b200 as vp
+
+    P = pre.params
+    chunk = max(1, min(args.e2e_chunk, per))
+    ring = max(chunk, min(2 * chunk, per))
+    clip_bytes = int(off[1] - off[0]) if per > 1 else int(frames.numel())
+    host = torch.empty(ring * clip_bytes, dtype=torch.uint8, pin_memory=True)
+    host.copy_(frames[: ring * clip_bytes].cpu())
+    grids_h = torch.empty_like(out["video_grid_thw"], device="cpu").pin_memory()
+    st_h = torch.empty_like(out["clip_status"], device="cpu").pin_memory()
+    dl_h = torch.empty_like(deltas, device="cpu").pin_memory()
+    rs_h = torch.empty_like(rst, device="cpu").pin_memory()
+    comp = torch.cuda.current_stream(dev)
+    copy = torch.cuda.Stream(dev)
+    h2d = per * clip_bytes
+    d2h = grids_h.numel() * 8 + st_h.numel() * 4 + dl_h.numel() * 8 + rs_h.numel() * 4
+
+    def step():
+        vp.plan_frames(P, pl.clips_dev, per, pl.plans_dev, pl.frame_indices, pl.totals_dev, pl.group_timestamps)
+        ev_plan = torch.cuda.Event()
+        ev_plan.record(comp)
+        done = []
+        for c0 in range(0, per, chunk):
+            c1 = min(per, c0 + chunk)
+            with torch.cuda.stream(copy):
+                if c0 == 0:
+                    copy.wait_event(ev_plan)        # previous step's kernels are done with these regions
+                for k in range(c0, c1):
+                    src = host[(k % ring) * clip_bytes: (k % ring + 1) * clip_bytes]
+                    frames[off[k]: off[k] + clip_bytes].copy_(src, non_blocking=True)
+                e = torch.cuda.Event()
+                e.record(copy)
+            comp.wait_event(e)
+            vp.resize_normalize_patchify(P, pl.plans_dev, c1 - c0, frames, torch_off, torch_pitch, None,
+                                         out["pixel_values_videos"], out["image_grid_thw"], out["video_grid_thw"],
+                                         out["clip_status"], stream=comp, first_clip=c0)
+            d = torch.cuda.Event()
+            d.record(comp)
+            done.append(d)
+        vp.rope_index(P, vp.VP_ROPE_QWEN3_SPLIT, tt, cu, None, out["video_grid_thw"], pos, deltas, rst, ws)
+        grids_h.copy_(out["video_grid_thw"], non_blocking=True)
+        st_h.copy_(out["clip_status"], non_blocking=True)
+        dl_h.copy_(deltas, non_blocking=True)
+        rs_h.copy_(rst, non_blocking=True)
+
+    torch_off = torch.from_numpy(off).to(dev)
+    torch_pitch = torch.from_numpy(pitch).to(dev)
+    for _ in range(max(1, args.warmup // 2)):
+        step()
+    torch.cuda.synchronize()
+    if world > 1:
+        dist.barrier()
+    a = torch.cuda.Event(enable_timing=True)
+    b = torch.cuda.Event(enable_timing=True)
+    a.record(comp)
+    for _ in range(args.e2e_steps):
+        step()
+    b.record(comp)
+    torch.cuda.synchronize()
+    ms = a.elapsed_time(b) / args.e2e_steps
+    t = torch.tensor([ms], dtype=torch.float64, device=dev)
+    if world > 1:
+        dist.all_reduce(t, op=dist.ReduceOp.MAX)
+    ms = float(t.item())
+    assert (st_h[:per].numpy() == 0).all()
+    return {"value": tokens_rank * world / (ms * 1e-3), "unit": UNIT, "h2d_bytes_per_step": h2d,
+            "d2h_bytes_per_step": d2h, "ms_per_step": ms, "steps": args.e2e_steps,
+            "path": "pinned host u8 frames -> H2D (copy stream, chunks of %d clips) overlapped with K3; "
+                    "D2H of grids/status/deltas" % chunk}
+
+
+# ----------------------------------------------------------------------------------------------
+# oracle (CPU baseline and the reference arm)
+# ----------------------------------------------------------------------------------------------
+
+def oracle_sample(frames_groups: int):
+    """The oracle, as it stands, on a bounded sample of the workload: one cfg5 clip's plan, its first
+    `frames_groups` temporal groups through resize/normalise/patchify, and the clip's MRoPE sequence
+    truncated to those groups.  Returns (visual tokens processed, seconds)."""
+    import oracle as O
+    import vp_inputs as I
+
+    params = cfg5_params()
+    c = cfg5_clip()
+    t0 = time.perf_counter()
+    pl = O.plan_clip(params, c)
+    tp, p, m = params["temporal_patch_size"], params["patch_size"], params["merge_size"]
+    g = min(frames_groups, pl.grid[0])
+    idx = pl.idx[: g * tp]
+    fr = I.frames_u8("noise", 0, idx, pl.in_h, pl.in_w)
+    gen = time.perf_counter() - t0
+    t0 = time.perf_counter()
+    res = np.stack([O.resize_frame(fr[k], pl.out_h, pl.out_w) for k in range(len(idx))])
+    rows = O.patchify(O.normalize(res, params["mean"], params["std"]), p, m, tp)
+    runs = [(0, 64)]
+    for _ in range(g):
+        runs += [(0, 7), (2, pl.grid[1] * pl.grid[2] // m ** 2), (0, 1)]
+    O.rope_index([I.token_types(runs)], [], [(g, pl.grid[1], pl.grid[2])], m)
+    secs = time.perf_counter() - t0
+    tokens = rows.shape[0] // (m * m)
+    return tokens, secs, gen
+
+
+def cpu_baseline(groups=4):
+    tokens, secs, _ = oracle_sample(groups)
+    cores = len(os.sched_getaffinity(0))
+    return {"value": tokens / secs, "unit": UNIT, "cores": cores, "kind": "oracle",
+            "sample": f"1 cfg5 clip, first {groups} temporal groups ({2 * groups} of 64 frames 720p->384x672) + "
+                      f"its MRoPE sequence; f64 numpy oracle (BLAS threads = host cores)",
+            "seconds": secs}
+
+
+def run_reference(args, rank, world):
+    if rank != 0:
+        return None
+    groups = max(1, args.ref_groups)
+    for _ in range(args.warmup):
+        oracle_sample(1)
+    times, toks = [], 0
+    for _ in range(args.steps):
+        tk, s, _ = oracle_sample(groups)
+        times.append(s)
+        toks = tk
+    v = toks / (sum(times) / len(times))
+    cores = len(os.sched_getaffinity(0))
+    sample = f"per step: 1 cfg5 clip, first {groups} temporal groups + MRoPE (f64 numpy oracle)"
+    return {"impl": "reference", "metric": METRIC, "value": v, "unit": UNIT, "n_gpus": world, "steps": args.steps,
+            "warmup": args.warmup, "ms_per_step": 1e3 * sum(times) / len(times), "higher_is_better": True,
+            "scaling": "strong", "vs_baseline": None, "dtype": "f64", "data": "synthetic",
+            "config": {"workload": "cfg5 (bounded oracle sample, see cpu_baseline.sample)"},
+            "cpu_baseline": {"value": v, "unit": UNIT, "cores": cores, "kind": "oracle", "sample": sample},
+            "e2e": {"value": v, "unit": UNIT, "h2d_bytes_per_step": 0, "d2h_bytes_per_step": 0}}
+
+
+def main():
+    ap = argparse.ArgumentParser()
+    ap.add_argument("--gpus", type=int, default=1)
+    ap.add_argument("--steps", type=int, default=10)
+    ap.add_argument("--warmup", type=int, default=3)
+    ap.add_argument("--impl", default="ours", choices=["ours", "reference"])
+    ap.add_argument("--clips", type=int, default=0, help="override job clip count (profiling only)")
+    ap.add_argument("--no-e2e", action="store_true")
+    ap.add_argument("--e2e-steps", type=int, default=2)
+    ap.add_argument("--e2e-chunk", type=int, default=8)
+    ap.add_argument("--no-cpu-baseline", action="store_true")
+    ap.add_argument("--cpu-groups", type=int, default=4)
+    ap.add_argument("--ref-groups", type=int, default=2)
+    args = ap.parse_args()
+    rank = int(os.environ.get("RANK", 0))
+    world = int(os.environ.get("WORLD_SIZE", 1))
+    local_rank = int(os.environ.get("LOCAL_RANK", 0))
+    if args.gpus != world and world == 1 and args.gpus > 1:
+        print(json.dumps({"error": "launch with torchrun for --gpus > 1"}))
+        sys.exit(2)
+    if args.impl == "reference":
+        r = run_reference(args, rank, world)
+        if r is not None:
+            print(json.dumps(r))
+        return
+    import torch
+    import torch.distributed as dist
+    if world > 1:
+        dist.init_process_group("nccl", device_id=torch.device("cuda", local_rank))
+    res = run_ours(args, rank, world, local_rank)
+    if rank == 0:
+        if world == 1 and not args.no_cpu_baseline:
+            res["cpu_baseline"] = cpu_baseline(args.cpu_groups)
+        print(json.dumps(res))
+    if world > 1:
+        dist.destroy_process_group()
+
+
+if __name__ == "__main__":
+    main()

@@ -380,15 +380,17 @@ def rope_index(seqs, image_grids, video_grids, merge: int, variant: int = 0, tim
     """seqs: list of 1-D int arrays of token types (0 text, 1 image, 2 video), one per sequence.
     image_grids / video_grids: lists of (t, h, w) in order of appearance across the batch.
     variant 0 (QWEN3_SPLIT): each video (t,h,w) is consumed as t grids (1,h,w) (C18).
-    variant 1 (QWEN2 classic): temporal id p + ti*time_interval (C19).
+    variant 1/2 (QWEN2 classic / QWEN25 time-scaled): temporal id p + ti*iv (C19); iv = time_interval,
+    an int or one value per video (QWEN25: tokens_per_second * int(second_per_grid_t), X: Qwen2.5-VL).
     Returns (ids list of int64 [3, L] arrays, deltas list, seq_status list, batch_status).
     A visual run whose length != t*(h/m)*(w/m), or with no grid left, is VP_EMISMATCH (C24, P:165);
     grids left unused at the end of the batch make batch_status VP_EMISMATCH."""
-    img = [tuple(int(v) for v in g) for g in image_grids]
+    img = [tuple(int(v) for v in g) + (1,) for g in image_grids]
     vid = []
-    for g in video_grids:
-        t, h, w = (int(v) for v in g)
-        vid += [(1, h, w)] * t if variant == 0 else [(t, h, w)]
+    for v, g in enumerate(video_grids):
+        t, h, w = (int(x) for x in g)
+        iv = time_interval[v] if isinstance(time_interval, (list, tuple)) else time_interval
+        vid += [(1, h, w, 1)] * t if variant == 0 else [(t, h, w, int(iv))]
     grids = {1: img, 2: vid}
     used = {1: 0, 2: 0}
     all_ids, deltas, status = [], [], []
@@ -413,12 +415,11 @@ def rope_index(seqs, image_grids, video_grids, merge: int, variant: int = 0, tim
                     used[typ] += 1
                     k = e
                     continue
-                t, h, w = grids[typ][used[typ]]
+                t, h, w, iv = grids[typ][used[typ]]
                 used[typ] += 1
                 hh, ww = h // merge, w // merge
                 if n != t * hh * ww:
                     st = VP_EMISMATCH
-                iv = time_interval
                 for j in range(min(n, t * hh * ww)):
                     ti, hi, wi = j // (hh * ww), (j // ww) % hh, j % ww
                     ids[0, k + j] = p + ti * iv

@@ -1,0 +1,168 @@
+"""GPU parity of K3 (vp_resize_normalize_patchify) against the f64 oracle (O4-O9).
+
+Element-by-element on small/ragged batches (several tiles + ragged tails, odd T, images, identity,
+up- and down-scale, misaligned pitches, fp32 and bf16), and on sampled outputs at the BASELINE
+sizes in the bench's launch configuration.  Tolerances: fp32 1e-5 absolute; bf16 reading C15."""
+import random
+
+import numpy as np
+import pytest
+import torch
+
+import oracle as O
+import vp_inputs as I
+from parity import assert_pixels, host_frames, oracle_params, pack_frames
+
+pytestmark = pytest.mark.gpu
+
+
+def _gpu_run(pre, clips, kind="noise", pitch_pad=0, frames=None):
+    pl = pre.plan(clips)
+    op = oracle_params(pre.params)
+    oplans, _ = O.plan_batch(op, clips)
+    fl = host_frames(oplans, kind) if frames is None else frames
+    pitches = [3 * c["width"] + pitch_pad for c in clips]
+    buf, offs, pit = pack_frames(fl, pitches)
+    out = pre.run(pl, buf, offs, pit)
+    torch.cuda.synchronize()
+    return pl, oplans, fl, out
+
+
+def _full_compare(pre, clips, kind="noise", pitch_pad=0):
+    pl, oplans, fl, out = _gpu_run(pre, clips, kind, pitch_pad)
+    op = oracle_params(pre.params)
+    ref = O.process_batch(op, clips, [f if f is not None else np.zeros((1, 1, 1, 3), np.uint8) for f in fl],
+                          plans=oplans)
+    st = out["clip_status"][: len(clips)].cpu().numpy()
+    assert st.tolist() == [p.status for p in oplans]
+    assert out["image_grid_thw"].cpu().numpy().tolist() == ref["image_grid_thw"].tolist()
+    assert out["video_grid_thw"].cpu().numpy().tolist() == ref["video_grid_thw"].tolist()
+    assert_pixels(out["pixel_values"].cpu(), ref["pixel_values_images"], "images")
+    assert_pixels(out["pixel_values_videos"].cpu(), ref["pixel_values_videos"], "videos")
+    return out
+
+
+@pytest.mark.parametrize("dtype", [1, 0])
+def test_cfg1_full(dtype):
+    import paper_2604_16893_b200 as vp
+    params, clips = I.config("cfg1")
+    params["out_dtype"] = dtype
+    out = _full_compare(vp.VisualPreprocessor(**params), clips, kind="ramp")
+    assert out["pixel_values_videos"].shape == (256, 1536)
+
+
+@pytest.mark.parametrize("dtype", [1, 0])
+def test_small_mixed_ragged_batch(dtype):
+    """Videos and images, odd T (temporal pad), identity / down / up scale on either axis."""
+    import paper_2604_16893_b200 as vp
+    pre = vp.VisualPreprocessor(max_frames=7, video_max_pixels=64 * 96, image_max_pixels=96 * 128, out_dtype=dtype)
+    clips = [I.clip(9, 2.0, 70, 100),          # n=7 (odd) -> pad; downscale
+             I.image(64, 96),                  # identity image -> tp copies
+             I.clip(3, 1.0, 20, 30),           # tiny -> upscale to 32x32
+             I.image(150, 40),                 # down rows, up cols
+             I.clip(6, 2.0, 64, 64),           # identity video (even n)
+             I.clip(0, 30.0, 64, 64),          # invalid: skipped
+             I.image(33, 257)]
+    _full_compare(pre, clips)
+
+
+@pytest.mark.parametrize("seed", range(4))
+def test_random_shapes_and_pitches(seed):
+    import paper_2604_16893_b200 as vp
+    rng = random.Random(100 + seed)
+    tp = rng.choice([1, 2, 3])
+    pre = vp.VisualPreprocessor(max_frames=max(tp, rng.choice([2, 3, 5])), temporal_patch_size=tp,
+                                patch_size=rng.choice([14, 16]), video_max_pixels=rng.choice([4096, 16384, 40000]),
+                                image_max_pixels=rng.choice([16384, 65536]), out_dtype=rng.choice([0, 1]),
+                                mean=(0.48145466, 0.4578275, 0.40821073), std=(0.26862954, 0.26130258, 0.27577711))
+    clips = []
+    for _ in range(rng.randint(1, 6)):
+        h, w = rng.randint(8, 600), rng.randint(8, 600)
+        clips.append(I.image(h, w) if rng.random() < 0.4 else I.clip(rng.randint(1, 40), rng.choice([2.0, 5.0]), h, w))
+    _full_compare(pre, clips, pitch_pad=rng.choice([0, 1, 5, 16]))
+
+
+def test_cfg2_one_clip_full():
+    """BASELINE cfg2 at full size, compared element by element (64 frames 720p -> 384x672)."""
+    import paper_2604_16893_b200 as vp
+    params, clips = I.config("cfg2")
+    params["out_dtype"] = 1
+    _full_compare(vp.VisualPreprocessor(**params), clips)
+
+
+def _sampled_compare(pre, clips, n_samples=4000, seed=0, kind="noise"):
+    """Full-size launch; the oracle computes sampled outputs one by one (resize_pixel)."""
+    pl, oplans, fl, out = _gpu_run(pre, clips, kind)
+    op = oracle_params(pre.params)
+    p, m, tp = op["patch_size"], op["merge_size"], op["temporal_patch_size"]
+    rng = np.random.default_rng(seed)
+    cache = {}
+    for mod, key in ((True, "pixel_values"), (False, "pixel_values_videos")):
+        pv = out[key]
+        sel = [o for o in oplans if o.status == O.VP_OK and o.is_image == mod]
+        if not sel:
+            continue
+        got_rows, ref_vals, gpu_vals = [], [], []
+        for _ in range(n_samples):
+            o = sel[rng.integers(len(sel))]
+            r = int(rng.integers(o.patches))
+            q = int(rng.integers(pv.shape[1]))
+            slot, y, x, c = O.patch_coords(r, q, o.grid, p, m, tp)
+            k = oplans.index(o)
+            fr = fl[k][min(slot, o.n - 1)]
+            v = O.resize_pixel(fr, o.out_h, o.out_w, y, x, c, cache)
+            ref_vals.append((v / 255.0 - op["mean"][c]) / op["std"][c])
+            got_rows.append((o.patch_offset + r, q))
+        idx = torch.tensor(got_rows, dtype=torch.int64, device=pv.device)
+        g = pv[idx[:, 0], idx[:, 1]].cpu()
+        assert_pixels(g, np.array(ref_vals), key)
+
+
+def test_cfg3_sampled():
+    import paper_2604_16893_b200 as vp
+    params, clips = I.config("cfg3")
+    _sampled_compare(vp.VisualPreprocessor(**params), clips, n_samples=3000)
+
+
+def test_cfg4_sampled():
+    import paper_2604_16893_b200 as vp
+    params, clips = I.config("cfg4")
+    _sampled_compare(vp.VisualPreprocessor(**params), clips, n_samples=3000)
+
+
+def test_determinism_three_runs():
+    """AC12: three runs are byte-identical."""
+    import paper_2604_16893_b200 as vp
+    params, clips = I.config("cfg4")
+    clips = clips[14:18]
+    pre = vp.VisualPreprocessor(**params)
+    outs = [_gpu_run(pre, clips)[3] for _ in range(3)]
+    for o in outs[1:]:
+        for k in ("pixel_values", "pixel_values_videos"):
+            assert torch.equal(o[k].view(torch.int16), outs[0][k].view(torch.int16))
+
+
+def test_capacity_is_reported_not_overrun():
+    import paper_2604_16893_b200 as vp
+    params, clips = I.config("cfg1")
+    pre = vp.VisualPreprocessor(**params)
+    pl = pre.plan(clips)
+    out = pre.alloc_outputs(pl)
+    big = torch.full((300, 1536), 7.0, dtype=torch.bfloat16, device="cuda")
+    out["pixel_values_videos"] = big[:100]               # needs 256 rows
+    fl = host_frames(O.plan_batch(oracle_params(pre.params), clips)[0])
+    buf, offs, pit = pack_frames(fl, [384])
+    pre.run(pl, buf, offs, pit, out=out)
+    assert out["clip_status"][0].item() == vp.VP_ECAPACITY
+    assert (big.float() == 7.0).all()
+
+
+def test_synth_frames_match_host_generator():
+    import paper_2604_16893_b200 as vp
+    for kind, kid in (("ramp", vp.VP_SYNTH_RAMP), ("noise", vp.VP_SYNTH_NOISE)):
+        ids = [3, 17, 1799]
+        H, W, pitch = 37, 53, 3 * 53 + 7
+        out = torch.zeros(len(ids) * H * pitch, dtype=torch.uint8, device="cuda")
+        vp.synth_frames(kid, 12345, torch.tensor(ids, device="cuda"), H, W, out, row_pitch=pitch)
+        got = out.cpu().numpy().reshape(len(ids), H, pitch)[:, :, : 3 * W].reshape(len(ids), H, W, 3)
+        assert np.array_equal(got, I.frames_u8(kind, 12345, ids, H, W))
