@@ -18,7 +18,7 @@ constexpr int kNScan = 10;
 enum { S_IDX = 0, S_IMGROWS, S_VIDROWS, S_IMGTOK, S_VIDTOK, S_NIMG, S_NVID, S_GROUPS, S_TILES, S_INVALID };
 
 struct ClipResult {
-  int32_t status, is_image, n, out_h, out_w, gt, gh, gw;
+  int32_t status, is_image, n, out_h, out_w, gt, gh, gw, variant;
   int64_t total;
   double src_fps, eff_fps;
 };
@@ -118,7 +118,12 @@ plan_kernel(vp_params P, const vp_clip_desc* __restrict__ clips, int n, vp_clip_
       v[r.is_image ? S_IMGTOK : S_VIDTOK] = patches / m2;
       v[r.is_image ? S_NIMG : S_NVID] = 1;
       v[S_GROUPS] = r.is_image ? 0 : r.gt;
-      v[S_TILES] = clip_tiles(r.gt, r.gh, r.gw, P.merge_size);
+      const int kv = select_variant(clips[k].height, clips[k].width, r.out_h, r.out_w);
+      r.variant = kv;
+      if (kv != KV_GENERIC) {
+        const int ws = fast_strip_width(clips[k].width, r.out_w, kv);
+        v[S_TILES] = (int64_t)r.n * ((r.out_w + ws - 1) / ws);     // items: frames x strips
+      }
     } else if (k < n) {
       v[S_INVALID] = 1;
     }
@@ -171,6 +176,7 @@ plan_kernel(vp_params P, const vp_clip_desc* __restrict__ clips, int n, vp_clip_
         pl.grid_index = r.is_image ? ex[S_NIMG] : ex[S_NVID];
         pl.group_offset = r.is_image ? 0 : ex[S_GROUPS];
         pl.tile_count = (int32_t)v[S_TILES];
+        pl.kernel_variant = r.variant;
         pl.effective_fps = r.eff_fps;
       }
       pl.index_offset = ex[S_IDX];

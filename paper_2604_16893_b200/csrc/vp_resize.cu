@@ -83,7 +83,7 @@ __device__ __forceinline__ void store_px(void* base, int64_t idx, float x) {
 // ------------------------------------------------------------------------------------------
 template <bool kF32>
 __global__ void __launch_bounds__(kThreads)
-resize_generic_kernel(KParams kp, const vp_clip_plan* __restrict__ plans, int n,
+resize_generic_kernel(KParams kp, const vp_clip_plan* __restrict__ plans, int n, int fast_aligned,
                       const uint8_t* __restrict__ frames, const int64_t* __restrict__ clip_off,
                       const int64_t* __restrict__ pitch_arr, void* pv_img, int64_t img_cap, void* pv_vid,
                       int64_t vid_cap) {
@@ -101,16 +101,23 @@ resize_generic_kernel(KParams kp, const vp_clip_plan* __restrict__ plans, int n,
 #define s_wv(r) (s_wv_base + (r) * kMaxTaps)
 #define s_wh(r) (s_wh_base + (r) * kMaxTaps)
 #define s_bad (*s_bad_p)
-  // tile range of this (sub-)batch: plans' tile_offset is a monotone prefix over the full batch
-  const int64_t tile_begin = plans[0].tile_offset;
-  const int64_t tile_end = plans[n - 1].tile_offset + plans[n - 1].tile_count;
+  // Clips this kernel owns: KV_GENERIC, or fast-variant clips whose buffers are not 16-B aligned
+  // (the fast kernel's TMA row copies need 16-B aligned rows).  Token tiles of every owned clip are
+  // dealt round-robin over the CTAs, continuing the rotation across clips.
   int cached_clip = -1;
-
-  for (int64_t tile = tile_begin + blockIdx.x; tile < tile_end; tile += gridDim.x) {
-    const int k = find_clip(plans, n, tile);
-    const vp_clip_plan pl = plans[k];
+  int64_t rot = 0;
+  for (int k = 0; k < n; ++k) {
+   const vp_clip_plan plk = plans[k];
+   if (plk.status != VP_OK) continue;
+   const bool fast_ok = fast_aligned && plk.kernel_variant != KV_GENERIC &&
+                        ((clip_off[k] | pitch_arr[k]) & 15) == 0;
+   if (fast_ok) continue;
+   const int64_t ntile = clip_tiles(plk.grid_t, plk.grid_h, plk.grid_w, kp.m);
+   const int64_t first = ((int64_t)blockIdx.x - rot % gridDim.x + gridDim.x) % gridDim.x;
+   rot += ntile;
+   for (int64_t local = first; local < ntile; local += gridDim.x) {
+    const vp_clip_plan& pl = plk;
     const int gh = pl.grid_h, gw = pl.grid_w;
-    const int64_t local = tile - pl.tile_offset;
     const int64_t tpg = (int64_t)(gh / m) * (gw / m);
     const int g = (int)(local / tpg);
     const int rem = (int)(local - (int64_t)g * tpg);
@@ -190,6 +197,7 @@ resize_generic_kernel(KParams kp, const vp_clip_plan* __restrict__ plans, int n,
       }
       ti = ti_end;
     }
+   }
   }
 #undef s_wv
 #undef s_wh
@@ -211,9 +219,9 @@ __global__ void grids_kernel(const vp_clip_plan* __restrict__ plans, int n, int6
       const int64_t rows = (int64_t)pl.grid_t * pl.grid_h * pl.grid_w;
       const bool img = pl.is_image;
       if (!(img ? has_img : has_vid) || pl.patch_offset + rows > (img ? img_cap : vid_cap)) st = VP_ECAPACITY;
-      // window length <= 4*max(in/out,1) + 2 taps must fit the weight tables (kMaxTaps)
+      // generic clips: window length <= 4*max(in/out,1) + 2 taps must fit the weight tables (kMaxTaps)
       const double fsv = fmax((double)pl.in_h / pl.out_h, 1.0), fsh = fmax((double)pl.in_w / pl.out_w, 1.0);
-      if (4.0 * fmax(fsv, fsh) + 2.0 > (double)kMaxTaps) st = VP_EUNSUPPORTED;
+      if (pl.kernel_variant == KV_GENERIC && 4.0 * fmax(fsv, fsh) + 2.0 > (double)kMaxTaps) st = VP_EUNSUPPORTED;
       int64_t* gptr = img ? img_grid : vid_grid;
       if (gptr != nullptr) {
         gptr[3 * pl.grid_index + 0] = pl.grid_t;
@@ -274,6 +282,10 @@ extern "C" vp_status vp_resize_normalize_patchify(const vp_params* p, const vp_c
   vp::grids_kernel<<<(n + 255) / 256, 256, 0, s>>>(plans, n, img_rows_cap, vid_rows_cap,
                                                    pixel_values_images != nullptr, pixel_values_videos != nullptr,
                                                    image_grid_thw, video_grid_thw, clip_status);
+  const int fast_aligned = (reinterpret_cast<uintptr_t>(frames) & 15) == 0;
+  if (fast_aligned)
+    vp::launch_resize_fast(p, plans, n, frames, clip_byte_offset, row_pitch, pixel_values_images, img_rows_cap,
+                           pixel_values_videos, vid_rows_cap, s);
   const int grid = vp::g_num_sms * 3;
   const size_t smem = vp::generic_smem_bytes(kp.m * kp.p);
   static bool attr_set = false;
@@ -283,11 +295,11 @@ extern "C" vp_status vp_resize_normalize_patchify(const vp_params* p, const vp_c
     attr_set = true;
   }
   if (kp.out_f32)
-    vp::resize_generic_kernel<true><<<grid, vp::kThreads, smem, s>>>(kp, plans, n, frames, clip_byte_offset,
+    vp::resize_generic_kernel<true><<<grid, vp::kThreads, smem, s>>>(kp, plans, n, fast_aligned, frames, clip_byte_offset,
                                                                    row_pitch, pixel_values_images, img_rows_cap,
                                                                    pixel_values_videos, vid_rows_cap);
   else
-    vp::resize_generic_kernel<false><<<grid, vp::kThreads, smem, s>>>(kp, plans, n, frames, clip_byte_offset,
+    vp::resize_generic_kernel<false><<<grid, vp::kThreads, smem, s>>>(kp, plans, n, fast_aligned, frames, clip_byte_offset,
                                                                     row_pitch, pixel_values_images, img_rows_cap,
                                                                     pixel_values_videos, vid_rows_cap);
   return vp::launch_status("vp_resize_normalize_patchify");

@@ -63,7 +63,7 @@ def test_cfg4_shaped_batch():
         seqs.append(I.token_types([(0, 64)] + _video_runs((32, 24, 42), m) + [(0, 32)]))
     img += [(1, 32, 48), (1, 16, 16)]
     vid.append((3, 16, 32))
-    seqs.append(I.token_types([(0, 5), (1, 96), (0, 3)] + _video_runs((3, 16, 32), m) + [(0, 2), (1, 16), (0, 9)]))
+    seqs.append(I.token_types([(0, 5), (1, 384), (0, 3)] + _video_runs((3, 16, 32), m) + [(0, 2), (1, 64), (0, 9)]))
     st, bst = _compare(seqs, img, vid, m)
     assert all(s == O.VP_OK for s in st) and bst == O.VP_OK
 
