@@ -44,55 +44,59 @@ constexpr int kTotLen = VP_TOT_LEN;
 
 // ------------------------------------------------------------------------------------------
 // Kernel-variant selection (plan time) for the fused resize.  The fast streaming kernel
-// (vp_resize_fast.cu) walks one source frame x one strip of output columns top to bottom:
-//   KV_MILD   : 4 consumer warps, 512-byte source footprint per row, <= 12 horizontal taps
-//   KV_STRONG : 8 consumer warps, 1024-byte footprint, <= 40 horizontal taps
-//   KV_GENERIC: everything else (vp_resize.cu generic kernel, token tiles)
-// A clip's "items" (tile_count) are n_frames x n_strips for the fast kernels, 0 for generic
-// (the generic kernel walks clips itself).  Everything here is integer / f64 exact.
+// (vp_resize_fast.cu) walks one source frame x one strip of output columns top to bottom with
+// 4 consumer warps of 8-byte lanes (1 KB source footprint per row); variants differ in the
+// horizontal tap bound:  KV_MILD <= 10 taps (fs_h < 2), KV_MEDIUM <= 20, KV_STRONG <= 40;
+// KV_GENERIC covers everything else (vp_resize.cu, token tiles).  A clip's items (tile_count)
+// are n_frames x n_strips for the fast variants, 0 for generic.  Integer / f64 exact.
 // ------------------------------------------------------------------------------------------
-enum { KV_MILD = 0, KV_STRONG = 1, KV_GENERIC = 2 };
-constexpr int kRing = 8;          // vertical ring slots (max live output rows per source row)
-constexpr int kInHMax = 2304;     // source rows supported by the fast kernel's per-row table
-constexpr int kWListMax = 8192;   // vertical weights (sum of window lengths) held in smem
-constexpr int kOutHMax = 4096;
+enum { KV_MILD = 0, KV_MEDIUM = 1, KV_STRONG = 2, KV_GENERIC = 3 };
+constexpr int kRing = 6;          // vertical ring slots (max live output rows per source row)
+constexpr int kInHMax = 1088;     // source rows supported by the fast kernel's per-row weight table
+constexpr int kWListMax = 6144;   // vertical weights (sum of window lengths) held in smem
+constexpr int kOutHMax = 2048;    // output rows (per-row tables; 12-bit index in the packed meta word)
+constexpr int kFastPx = 512;      // source footprint pixels per row (4 V warps x 32 lanes x 4 px)
+constexpr int kFastMaxWs = 256;   // strip width bound: column pairs <= 128 H threads
 
-__host__ __device__ __forceinline__ int fast_fpb(int variant) { return variant == KV_MILD ? 512 : 1024; }
-__host__ __device__ __forceinline__ int fast_lhm(int variant) { return variant == KV_MILD ? 12 : 40; }
+__host__ __device__ __forceinline__ int fast_lhm(int variant) {
+  return variant == KV_MILD ? 9 : (variant == KV_MEDIUM ? 18 : 40);
+}
 
 // max window length (taps) of an in->out axis: x1-x0 <= 2*support+1 (+1 for truncation slack)
 __host__ __device__ __forceinline__ int axis_max_taps(int in, int out) {
+  if (in == out) return 1;          // identity axis: weights are exactly {0,..,1,..,0}; zero taps are trimmed
   double s = (double)in / (double)out;
   double fs = s > 1.0 ? s : 1.0;
   return (int)floor(4.0 * fs) + 2;
 }
 
-// Output-column strip width for a fast variant: the largest multiple of 16 whose source footprint
-// (<= (Ws-1)*s + taps + 1 pixels, plus 15 bytes of 16-byte alignment slack) fits fpb bytes.
-__host__ __device__ __forceinline__ int fast_strip_width(int in_w, int out_w, int variant) {
+// Strip width: the footprint of any Ws consecutive output columns, started at a 16-pixel boundary
+// (<= 15 + (Ws-1)*s + taps + 1 pixels) must fit kFastPx.  Strips are balanced: n = ceil(out_w / Wmax),
+// Ws = roundup16(ceil(out_w / n)).  Returns 0 if no 16-wide strip fits.
+__host__ __device__ __forceinline__ int fast_strip_width(int in_w, int out_w) {
   const double s = (double)in_w / (double)out_w;
   const int taps = axis_max_taps(in_w, out_w);
-  const int fpb = fast_fpb(variant);
-  int ws = 0;
-  for (int cand = 16; cand <= out_w + 15; cand += 16) {
-    double px = (cand - 1) * s + taps + 1;
-    if (3.0 * px + 15.0 <= (double)fpb) ws = cand; else break;
+  int wmax = 0;
+  for (int cand = 16; cand <= kFastMaxWs; cand += 16) {
+    if (15.0 + (cand - 1) * s + taps + 1.0 <= (double)kFastPx) wmax = cand; else break;
   }
-  const int maxws = 80;   // (col, channel) units per strip <= consumer threads x units/thread (both variants)
-  if (ws > maxws) ws = maxws;
+  if (wmax == 0) return 0;
+  const int nstrips = (out_w + wmax - 1) / wmax;
+  int ws = (out_w + nstrips - 1) / nstrips;
+  ws = (ws + 15) & ~15;
   if (ws > out_w) ws = out_w;
   return ws;
 }
 
 __host__ __device__ __forceinline__ int select_variant(int in_h, int in_w, int out_h, int out_w) {
   const double sv = (double)in_h / (double)out_h;
-  if (sv < 0.6 || in_h > kInHMax || out_h > kOutHMax) return KV_GENERIC;       // ring needs <= 8 live rows
-  if ((int64_t)out_h * axis_max_taps(in_h, out_h) > kWListMax) return KV_GENERIC;
+  // live output rows per source row <= ceil(4 / s) for upscale, <= 5 for downscale: s >= 0.67 fits 6 slots
+  if (sv < 0.67 || in_h > kInHMax || out_h > kOutHMax) return KV_GENERIC;
   const double sh = (double)in_w / (double)out_w;
-  if (sh < 0.6) return KV_GENERIC;
+  if (sh < 0.6 || fast_strip_width(in_w, out_w) < 16) return KV_GENERIC;
   const int th = axis_max_taps(in_w, out_w);
-  if (th <= fast_lhm(KV_MILD) && fast_strip_width(in_w, out_w, KV_MILD) >= 16) return KV_MILD;
-  if (th <= fast_lhm(KV_STRONG) && fast_strip_width(in_w, out_w, KV_STRONG) >= 16) return KV_STRONG;
+  for (int v = KV_MILD; v <= KV_STRONG; ++v)
+    if (th <= fast_lhm(v)) return v;
   return KV_GENERIC;
 }
 

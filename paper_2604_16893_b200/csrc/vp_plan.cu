@@ -121,7 +121,7 @@ plan_kernel(vp_params P, const vp_clip_desc* __restrict__ clips, int n, vp_clip_
       const int kv = select_variant(clips[k].height, clips[k].width, r.out_h, r.out_w);
       r.variant = kv;
       if (kv != KV_GENERIC) {
-        const int ws = fast_strip_width(clips[k].width, r.out_w, kv);
+        const int ws = fast_strip_width(clips[k].width, r.out_w);
         v[S_TILES] = (int64_t)r.n * ((r.out_w + ws - 1) / ws);     // items: frames x strips
       }
     } else if (k < n) {

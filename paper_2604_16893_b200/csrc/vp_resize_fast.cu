@@ -1,31 +1,39 @@
 // vp_resize_fast.cu -- K3 fast path: streaming fused AA-bicubic resize + clamp + normalise +
-// temporal pad + patchify (O4-O9) for the common ratios (KV_MILD / KV_STRONG, see vp_internal.cuh).
+// temporal pad + patchify (O4-O9) for the common ratios (KV_MILD / KV_MEDIUM / KV_STRONG).
 //
-// Work item = (clip, source frame f, strip of Ws output columns); a CTA walks the item's source
-// rows top to bottom once:
-//   * producer warp: streams each source row's footprint bytes (16-B aligned, <= 512 / 1024 B) into a
-//     16-slot shared-memory ring with cp.async.bulk (TMA bulk copy) + mbarrier complete_tx, running
-//     ahead across items;
-//   * NCW consumer warps, vertical pass: lane L owns 4 consecutive footprint bytes; every source row is
-//     read from smem once (LDS.32), converted once (I2F.U8) and FMA'd (FFMA2) into the <= 8 live output
-//     rows held in a register ring acc[8] -- uniform per-row control (meta[y]: first live row, live
-//     count, retiring count) dispatched with one jump-table switch per row, so no dynamic register
-//     indexing and no wasted FMAs;
-//   * retired output rows (fp32, footprint-wide) go to a small smem buffer; every 4 rows the consumers
-//     run the horizontal pass (weights in registers for MILD), clamp, normalise (one FFMA), round to
-//     bf16/f32 and store straight into the HF patch layout -- every output element written once, to
-//     every temporal slot the frame fills (odd-n padding, images).
-// Tables (per clip, cached across a CTA's consecutive items): vertical windows as a compact
-// per-source-row list (meta + weights), weights computed in f64 and stored fp32.
+// Work item = (clip, source frame f, strip of Ws <= 256 output columns).  A CTA walks the item's
+// source rows top to bottom exactly once with two warp-specialised groups:
+//   * 4 V warps (vertical pass).  Each V warp owns a 128-pixel (384-byte) slice of the strip's
+//     source footprint and is its own TMA producer: lane 0 keeps kDepth rows of its slice in flight
+//     with cp.async.bulk (global -> smem, completion on a per-warp mbarrier); lane L converts its 4
+//     pixels (12 bytes, I2F.U8) once per source row and FMAs them (FFMA2) into the <= 8 output rows
+//     live at that row, held in a register ring acc[6].  Output row i lives in slot i % 6; the
+//     output-row loop is unrolled by 6 so every slot index is static (no dynamic register indexing,
+//     no accumulator shuffles), and each source row dispatches once on its live count.
+//   * 4 H warps (horizontal pass).  Retired rows arrive through a 4-row smem buffer, pixel-major
+//     (float4 = RGB + pad) with mbarrier hand-off; each H thread computes 2 adjacent output columns x
+//     2 rows x 3 channels (LDS.128 + FFMA2, horizontal weights in registers for MILD), clamps,
+//     normalises and stores bf16x2 / float2 straight into the HF patch layout, once per temporal slot
+//     the frame fills (O7) -- every output element is written exactly once.
+// Registers are rebalanced between the warpgroups with setmaxnreg (V holds the 72-register ring).
+// Per-clip tables (cached across a CTA's consecutive items): per source row an aligned 8-float vector
+// of the weights of its live output rows + the live count (fp32 from f64); windows are trimmed of
+// exact-zero taps (identity axes become 1-tap copies).  Per item: the strip's horizontal weights.
+// The V warps load row y+1's staged bytes and weight vector while FMA-ing row y (software pipeline).
 #include "vp_internal.cuh"
 #include <cuda_bf16.h>
 
 namespace vp {
 namespace {
 
-constexpr int kSlots = 16;        // source-row ring depth (TMA in flight)
-constexpr int kCapR = 8;          // retired-row buffer (rows)
-constexpr int kQH = 4;            // horizontal pass every 4 retired rows
+constexpr int kNVW = 4;                   // V warps
+constexpr int kNHW = 4;                   // H warps
+constexpr int kNT = (kNVW + kNHW) * 32;   // 256 threads
+constexpr int kDepth = 8;                 // source rows in flight per V warp
+constexpr int kWarpPx = 128;              // pixels per V warp slice (32 lanes x 4 px)
+constexpr int kWarpB = 3 * kWarpPx;       // 384 bytes
+constexpr int kCapR = 4;                  // retired-row buffer rows (V -> H)
+constexpr int kRowPx = kFastPx + 48;      // float4 pixels per buffered row (+ tap slack)
 
 struct FKParams {
   int p, m, tp, D;
@@ -77,7 +85,8 @@ __device__ __forceinline__ double keys_d(double x) {
   return 0.0;
 }
 
-// Window of output index i on an in->out axis (C10): x0, x1 (exclusive), centre c, 1/fs.
+// Window of output index i on an in->out axis (C10), trimmed of exact-zero end taps (zero taps add
+// exactly 0 to the sum; trimming makes identity axes 1-tap).  x0, x1 (exclusive), centre c, 1/fs.
 struct Win {
   int x0, x1;
   double c, inv;
@@ -93,6 +102,8 @@ __device__ __forceinline__ Win window_of(int in, int out, int i) {
   if (w.x0 < 0) w.x0 = 0;
   w.x1 = (int)(w.c + support + 0.5);
   if (w.x1 > in) w.x1 = in;
+  while (w.x1 - w.x0 > 1 && keys_d(((double)w.x0 - w.c + 0.5) * w.inv) == 0.0) ++w.x0;
+  while (w.x1 - w.x0 > 1 && keys_d(((double)(w.x1 - 1) - w.c + 0.5) * w.inv) == 0.0) --w.x1;
   return w;
 }
 
@@ -105,144 +116,181 @@ __device__ __forceinline__ int find_clip_f(const vp_clip_plan* __restrict__ plan
   return lo;
 }
 
-// Item decode shared by producer and consumers.
-struct Item {
-  int k;            // clip
-  int f;            // source frame
-  int strip, ws, j0, jn;   // strip index, strip width, first column, columns in this strip
-  int64_t clip_end; // first item after this clip
-  bool mine;
-};
-
 __device__ __forceinline__ bool clip_is_mine(const vp_clip_plan& pl, int variant, int64_t coff, int64_t pitch) {
   return pl.status == VP_OK && pl.kernel_variant == variant && ((coff | pitch) & 15) == 0 && pl.tile_count > 0;
 }
 
-// ---------------------------------------------------------------- the vertical ring (switch dispatch)
-// acc[r] = {bytes 0,1} and acc[r+8] = {bytes 2,3} of output row in slot r (slot = row & 7)
-#define VP_FMA2(A, W, F)                                                       \
-  asm("fma.rn.f32x2 %0, %1, %2, %0;" : "+l"(A) : "l"(F), "l"(W))
+// Footprint of a strip: first pixel (16-aligned so that the byte offset 3*pa is 16-B aligned for TMA)
+// and pixel count.
+struct Strip {
+  int j0, jn, pa, np;
+};
+__device__ __forceinline__ Strip strip_of(const vp_clip_plan& pl, int ws, int strip) {
+  Strip s;
+  s.j0 = strip * ws;
+  s.jn = min(ws, pl.out_w - s.j0);
+  s.pa = window_of(pl.in_w, pl.out_w, s.j0).x0 & ~15;
+  s.np = window_of(pl.in_w, pl.out_w, s.j0 + s.jn - 1).x1 - s.pa;
+  return s;
+}
 
-__device__ __forceinline__ unsigned long long pack2(float a, float b) {
-  unsigned long long r;
-  asm("mov.b64 %0, {%1,%2};" : "=l"(r) : "f"(a), "f"(b));
-  return r;
-}
-__device__ __forceinline__ float2 unpack2(unsigned long long v) {
-  float2 r;
-  asm("mov.b64 {%0,%1}, %2;" : "=f"(r.x), "=f"(r.y) : "l"(v));
-  return r;
-}
+
+// ---------------------------------------------------------------- vertical ring
+// acc[slot][q]: bytes (2q, 2q+1) of this lane's 12 source bytes (4 RGB pixels) for the output row in
+// `slot` (= row & 7).
+typedef float2 Acc[kRing][6];
 
 template <int BASE, int CNT>
-__device__ __forceinline__ void ring_contrib(unsigned long long (&acc)[16], const float* __restrict__ w,
-                                             unsigned long long f01, unsigned long long f23) {
+__device__ __forceinline__ void ring_contrib(Acc& acc, const float* __restrict__ w, const float2 (&f)[6]) {
 #pragma unroll
   for (int r = 0; r < CNT; ++r) {
-    constexpr int dummy = 0;
-    (void)dummy;
-    const int slot = (BASE + r) & 7;
+    const int slot = (BASE + r) % kRing;
     const float wr = w[r];
-    const unsigned long long ww = pack2(wr, wr);
-    VP_FMA2(acc[slot], ww, f01);
-    VP_FMA2(acc[slot + 8], ww, f23);
-  }
-}
-
-#define VP_RC(B)                                                              \
-  case B * 16 + 0: break;                                                     \
-  case B * 16 + 1: ring_contrib<B, 1>(acc, w, f01, f23); break;               \
-  case B * 16 + 2: ring_contrib<B, 2>(acc, w, f01, f23); break;               \
-  case B * 16 + 3: ring_contrib<B, 3>(acc, w, f01, f23); break;               \
-  case B * 16 + 4: ring_contrib<B, 4>(acc, w, f01, f23); break;               \
-  case B * 16 + 5: ring_contrib<B, 5>(acc, w, f01, f23); break;               \
-  case B * 16 + 6: ring_contrib<B, 6>(acc, w, f01, f23); break;               \
-  case B * 16 + 7: ring_contrib<B, 7>(acc, w, f01, f23); break;               \
-  case B * 16 + 8: ring_contrib<B, 8>(acc, w, f01, f23); break;
-
-__device__ __forceinline__ void ring_step(unsigned long long (&acc)[16], int code, const float* __restrict__ w,
-                                          unsigned long long f01, unsigned long long f23) {
-  switch (code) {
-    VP_RC(0) VP_RC(1) VP_RC(2) VP_RC(3) VP_RC(4) VP_RC(5) VP_RC(6) VP_RC(7)
-    default: break;
-  }
-}
-
-template <int BASE, int NRET>
-__device__ __forceinline__ void ring_retire(unsigned long long (&acc)[16], float* __restrict__ vbuf, int row0,
-                                            int fpf, int lane_f, bool active) {
+    const float2 ww = make_float2(wr, wr);
 #pragma unroll
-  for (int r = 0; r < NRET; ++r) {
-    const int slot = (BASE + r) & 7;
-    if (active) {
-      float2 a = unpack2(acc[slot]), b = unpack2(acc[slot + 8]);
-      float4* dst = reinterpret_cast<float4*>(vbuf + ((row0 + r) & (kCapR - 1)) * fpf + lane_f);
-      *dst = make_float4(a.x, a.y, b.x, b.y);
-    }
-    acc[slot] = 0ull;
-    acc[slot + 8] = 0ull;
+    for (int q = 0; q < 6; ++q) acc[slot][q] = __ffma2_rn(ww, f[q], acc[slot][q]);
   }
 }
 
-#define VP_RR(B)                                                                  \
-  case B * 4 + 1: ring_retire<B, 1>(acc, vbuf, row0, fpf, lane_f, active); break; \
-  case B * 4 + 2: ring_retire<B, 2>(acc, vbuf, row0, fpf, lane_f, active); break; \
-  case B * 4 + 3: ring_retire<B, 3>(acc, vbuf, row0, fpf, lane_f, active); break;
-
-__device__ __forceinline__ void ring_retire_dispatch(unsigned long long (&acc)[16], int code, float* __restrict__ vbuf,
-                                                     int row0, int fpf, int lane_f, bool active) {
-  switch (code) {
-    VP_RR(0) VP_RR(1) VP_RR(2) VP_RR(3) VP_RR(4) VP_RR(5) VP_RR(6) VP_RR(7)
+// contributions of one source row to the live rows i..i+cnt-1, where row i sits in slot U (static)
+template <int U>
+__device__ __forceinline__ void ring_row(Acc& acc, int cnt, const float* __restrict__ w, const float2 (&f)[6]) {
+  switch (cnt) {
+    case 1: ring_contrib<U, 1>(acc, w, f); break;
+    case 2: ring_contrib<U, 2>(acc, w, f); break;
+    case 3: ring_contrib<U, 3>(acc, w, f); break;
+    case 4: ring_contrib<U, 4>(acc, w, f); break;
+    case 5: ring_contrib<U, 5>(acc, w, f); break;
+    case 6: ring_contrib<U, 6>(acc, w, f); break;
     default: break;
   }
 }
 
-// ---------------------------------------------------------------- kernel
-template <int VARIANT, bool kF32>
+// store the finished output row of slot S as 4 pixel-major float4 (RGB + pad) and clear the slot
+template <int S>
+__device__ __forceinline__ void retire_slot(Acc& acc, float4* __restrict__ dst, bool active) {
+  if (active) {
+    const float2* a = acc[S];
+    dst[0] = make_float4(a[0].x, a[0].y, a[1].x, 0.f);
+    dst[1] = make_float4(a[1].y, a[2].x, a[2].y, 0.f);
+    dst[2] = make_float4(a[3].x, a[3].y, a[4].x, 0.f);
+    dst[3] = make_float4(a[4].y, a[5].x, a[5].y, 0.f);
+  }
+#pragma unroll
+  for (int q = 0; q < 6; ++q) acc[S][q] = make_float2(0.f, 0.f);
+}
+
+template <bool kF32>
+__device__ __forceinline__ void store_slots(void* pv, int64_t idx, float v0, float v1, int nslots, int ti0, int tp,
+                                            int p, int64_t group_stride) {
+  for (int s2 = 0, ti = ti0; s2 < nslots; ++s2) {
+    if (kF32) *reinterpret_cast<float2*>(reinterpret_cast<float*>(pv) + idx) = make_float2(v0, v1);
+    else *reinterpret_cast<__nv_bfloat162*>(reinterpret_cast<__nv_bfloat16*>(pv) + idx) = __floats2bfloat162_rn(v0, v1);
+    if (++ti == tp) { ti = 0; idx += group_stride - (int64_t)(tp - 1) * p * p; }
+    else idx += (int64_t)p * p;
+  }
+}
+
+// ---------------------------------------------------------------- configuration per variant
+template <int VARIANT>
 struct FastCfg {
-  static constexpr int NCW = VARIANT == KV_MILD ? 4 : 8;           // consumer warps
-  static constexpr int NC = NCW * 32;                               // consumer threads
-  static constexpr int FPB = VARIANT == KV_MILD ? 512 : 1024;       // footprint bytes per row
-  static constexpr int LHM = VARIANT == KV_MILD ? 12 : 40;          // horizontal taps bound
-  static constexpr bool HREG = VARIANT == KV_MILD;                  // horizontal weights in registers
-  static constexpr int UPT = VARIANT == KV_MILD ? 2 : 1;            // max (col,channel) units per thread
-  static constexpr int MAXWS = (UPT * NC) / 3;                      // strip width bound from units
-  static constexpr int VPAD = 3 * LHM + 16;                         // slack after each V row (floats)
-  static constexpr int FPF = FPB + VPAD;                            // floats per retired row
-  // smem layout (bytes)
-  static constexpr size_t OFF_RING = 0;                                                   // kSlots*FPB u8
-  static constexpr size_t OFF_VBUF = OFF_RING + (size_t)kSlots * FPB;                     // kCapR*FPF f32
-  static constexpr size_t OFF_META = OFF_VBUF + (size_t)kCapR * FPF * 4;                  // kInHMax int2
-  static constexpr size_t OFF_WL = OFF_META + (size_t)kInHMax * 8;                        // kWListMax f32
-  static constexpr size_t OFF_WH = OFF_WL + (size_t)kWListMax * 4;                        // MAXWS*LHM f32
-  static constexpr size_t OFF_HX = OFF_WH + (size_t)MAXWS * LHM * 4;                      // MAXWS int
-  static constexpr size_t OFF_BAR = (OFF_HX + (size_t)MAXWS * 4 + 15) & ~(size_t)15;     // 2*kSlots u64
-  static constexpr size_t OFF_MISC = OFF_BAR + 2 * kSlots * 8;
-  static constexpr size_t SMEM = OFF_MISC + 64;
+  static constexpr int LHM = VARIANT == KV_MILD ? 9 : (VARIANT == KV_MEDIUM ? 18 : 40);
+  static constexpr bool HREG = false;                    // horizontal weights: one LDS.64 per tap (both columns)
+  // strips: 15 + (Ws-1)*fs + taps + 1 <= kFastPx with fs >= 4 for STRONG -> Ws <= 128
+  static constexpr int MAXWS = VARIANT == KV_STRONG ? 128 : kFastMaxWs;
+  static constexpr size_t OFF_STG = 0;                                                   // V staging
+  static constexpr size_t OFF_VBUF = OFF_STG + (size_t)kNVW * kDepth * kWarpB;          // retired rows
+  static constexpr size_t OFF_WROW = OFF_VBUF + (size_t)kCapR * kRowPx * 16;
+  static constexpr size_t OFF_SCR = OFF_WROW + (size_t)kInHMax * 32;
+  static constexpr size_t OFF_Y1 = OFF_SCR + (size_t)kOutHMax * 4;
+  static constexpr size_t OFF_WH = OFF_Y1 + (size_t)kOutHMax * 4;
+  static constexpr size_t OFF_HX = OFF_WH + (size_t)MAXWS * LHM * 4;
+  static constexpr size_t OFF_BAR = (OFF_HX + (size_t)MAXWS * 4 + 15) & ~(size_t)15;
+  static constexpr size_t SMEM = OFF_BAR + (kNVW * kDepth + 2 * kCapR) * 8;
+  static_assert(OFF_VBUF % 16 == 0 && OFF_WROW % 16 == 0 && OFF_WH % 16 == 0, "align");
+};
+
+// Per-V-warp TMA producer (lane 0): walks the CTA's item sequence and keeps its slice of kDepth rows
+// in flight.  issue() refills the slot of the row the warp has just finished reading.
+template <int VARIANT>
+struct Producer {
+  const vp_clip_plan* plans;
+  int n, w;
+  const uint8_t* frames;
+  const int64_t* clip_off;
+  const int64_t* pitch_arr;
+  int64_t item, my_b, cend;
+  int y, in_h, nbytes;
+  int64_t pitch;
+  const uint8_t* src;
+  bool live;
+
+  __device__ __noinline__ void open_item() {
+    while (item < my_b) {
+      const int k = find_clip_f(plans, n, item);
+      const vp_clip_plan pl = plans[k];
+      cend = pl.tile_offset + pl.tile_count;
+      const int64_t coff = clip_off[k];
+      pitch = pitch_arr[k];
+      if (!clip_is_mine(pl, VARIANT, coff, pitch)) {
+        item = cend;
+        continue;
+      }
+      const int ws = fast_strip_width(pl.in_w, pl.out_w);
+      const int nstrips = (pl.out_w + ws - 1) / ws;
+      const int64_t local = item - pl.tile_offset;
+      const int f = (int)(local / nstrips), strip = (int)(local % nstrips);
+      const Strip st = strip_of(pl, ws, strip);
+      const int px0 = st.pa + w * kWarpPx;                       // this warp's first pixel
+      const int pxn = min(kWarpPx, st.pa + st.np - px0);         // its pixels (may be <= 0)
+      // 16-B multiple, never past the 16-B rounded row end (pitch is a multiple of 16 >= 3*in_w)
+      nbytes = pxn > 0 ? min(kWarpB, (3 * (px0 + pxn) + 15) / 16 * 16 - 3 * px0) : 0;
+      src = frames + coff + (int64_t)f * pl.in_h * pitch + 3 * (int64_t)px0;
+      in_h = pl.in_h;
+      y = 0;
+      live = true;
+      return;
+    }
+    live = false;
+  }
+  __device__ __forceinline__ void issue(uint8_t* stage, uint64_t* full, uint32_t slot) {
+    if (!live) return;
+    if (nbytes > 0) {
+      mbar_arrive_expect_tx(&full[slot], (uint32_t)nbytes);
+      tma_bulk_g2s(stage + (size_t)slot * kWarpB, src + (int64_t)y * pitch, (uint32_t)nbytes, &full[slot]);
+    } else {
+      mbar_arrive(&full[slot]);                                   // empty slice: complete the phase
+    }
+    if (++y == in_h) {
+      ++item;
+      open_item();
+    }
+  }
 };
 
 template <int VARIANT, bool kF32>
-__global__ void __launch_bounds__(FastCfg<VARIANT, kF32>::NC + 32)
+__global__ void __launch_bounds__(kNT, 2)
 resize_fast_kernel(FKParams kp, const vp_clip_plan* __restrict__ plans, int n, const uint8_t* __restrict__ frames,
                    const int64_t* __restrict__ clip_off, const int64_t* __restrict__ pitch_arr, void* pv_img,
                    int64_t img_cap, void* pv_vid, int64_t vid_cap) {
-  using Cfg = FastCfg<VARIANT, kF32>;
+  using Cfg = FastCfg<VARIANT>;
+  constexpr int LHM = Cfg::LHM;
   extern __shared__ __align__(128) unsigned char smem[];
-  uint8_t* ring = smem + Cfg::OFF_RING;
-  float* vbuf = reinterpret_cast<float*>(smem + Cfg::OFF_VBUF);
-  int2* meta = reinterpret_cast<int2*>(smem + Cfg::OFF_META);
-  float* wl = reinterpret_cast<float*>(smem + Cfg::OFF_WL);
+  uint8_t* stage_all = smem + Cfg::OFF_STG;
+  float4* vbuf = reinterpret_cast<float4*>(smem + Cfg::OFF_VBUF);
+  float* wrow = reinterpret_cast<float*>(smem + Cfg::OFF_WROW);     // [kInHMax][8] vertical weights
+  float* vscratch = reinterpret_cast<float*>(smem + Cfg::OFF_SCR);  // [kOutHMax] table-build scratch
+  int* y1t = reinterpret_cast<int*>(smem + Cfg::OFF_Y1);
   float* wh = reinterpret_cast<float*>(smem + Cfg::OFF_WH);
   int* hx = reinterpret_cast<int*>(smem + Cfg::OFF_HX);
-  uint64_t* full = reinterpret_cast<uint64_t*>(smem + Cfg::OFF_BAR);
-  uint64_t* empty = full + kSlots;
-  int* misc = reinterpret_cast<int*>(smem + Cfg::OFF_MISC);
+  uint64_t* full_all = reinterpret_cast<uint64_t*>(smem + Cfg::OFF_BAR);   // [kNVW][kDepth]
+  uint64_t* vfull = full_all + kNVW * kDepth;                               // retired rows: V -> H
+  uint64_t* vempty = vfull + kCapR;                                         // H -> V
 
   const int tid = threadIdx.x;
-  const int warp = tid >> 5;
-  const bool producer = warp == Cfg::NCW;
+  const int warp = tid >> 5, lane = tid & 31;
 
-  // item range of this CTA (contiguous slice of the batch's fast-item space)
+  // contiguous slice of the batch's fast-item space
   const int64_t it_begin = plans[0].tile_offset;
   const int64_t it_end = plans[n - 1].tile_offset + plans[n - 1].tile_count;
   const int64_t total = it_end - it_begin;
@@ -250,275 +298,308 @@ resize_fast_kernel(FKParams kp, const vp_clip_plan* __restrict__ plans, int n, c
   const int64_t my_b = it_begin + total * (blockIdx.x + 1) / gridDim.x;
 
   if (tid == 0) {
-    for (int s = 0; s < kSlots; ++s) {
-      mbar_init(&full[s], 1);
-      mbar_init(&empty[s], Cfg::NCW);
+    for (int s = 0; s < kNVW * kDepth; ++s) mbar_init(&full_all[s], 1);
+    for (int s = 0; s < kCapR; ++s) {
+      mbar_init(&vfull[s], kNVW);
+      mbar_init(&vempty[s], kNHW);
     }
     asm volatile("fence.mbarrier_init.release.cluster;" ::: "memory");
   }
-  for (int i = tid; i < kCapR * Cfg::FPF; i += blockDim.x) vbuf[i] = 0.f;
+  for (int i = tid; i < kCapR * kRowPx; i += kNT) vbuf[i] = make_float4(0.f, 0.f, 0.f, 0.f);
   __syncthreads();
 
-  if (producer) {
-    // ------------------------------------------------------------ producer: TMA bulk row streaming
-    if ((tid & 31) != 0) return;
-    uint32_t slot = 0, phase = 0;
+  if (warp < kNVW) {
+    // ============================================================ V warps: vertical ring
+    asm volatile("setmaxnreg.inc.sync.aligned.u32 152;\n" ::: "memory");
+    uint8_t* stage = stage_all + (size_t)warp * kDepth * kWarpB;
+    uint64_t* full = full_all + warp * kDepth;
+    uint32_t rslot = 0, rphase = 0;   // staging ring position of the next row to read
+    uint32_t vrow = 0;                // running count of retired rows (vbuf slot = vrow % kCapR)
+    int cached_clip = -1;
+    Producer<VARIANT> pr;
+    if (lane == 0) {
+      pr.plans = plans; pr.n = n; pr.w = warp; pr.frames = frames; pr.clip_off = clip_off;
+      pr.pitch_arr = pitch_arr; pr.item = my_a; pr.my_b = my_b;
+      pr.open_item();
+      for (uint32_t q = 0; q < kDepth; ++q) pr.issue(stage, full, q);     // prefill
+    }
     int64_t item = my_a;
     while (item < my_b) {
       const int k = find_clip_f(plans, n, item);
       const vp_clip_plan pl = plans[k];
       const int64_t cend = pl.tile_offset + pl.tile_count;
-      const int64_t coff = clip_off[k], pitch = pitch_arr[k];
-      if (!clip_is_mine(pl, VARIANT, coff, pitch)) {
+      if (!clip_is_mine(pl, VARIANT, clip_off[k], pitch_arr[k])) {
         item = cend;
         continue;
       }
-      const int ws = fast_strip_width(pl.in_w, pl.out_w, VARIANT);
+      const int ws = fast_strip_width(pl.in_w, pl.out_w);
       const int nstrips = (pl.out_w + ws - 1) / ws;
+      const int in_h = pl.in_h, out_h = pl.out_h;
+      if (k != cached_clip) {
+        // ---- vertical tables for this clip (K2), V warps only ----
+        float* invs = reinterpret_cast<float*>(vscratch);   // 1/sum scratch (out_h floats)
+        named_sync(1, kNVW * 32);
+        for (int i = tid; i < out_h; i += kNVW * 32) {
+          const Win w = window_of(in_h, out_h, i);
+          y1t[i] = w.x1;
+          double s = 0.0;
+          for (int y = w.x0; y < w.x1; ++y) s += keys_d(((double)y - w.c + 0.5) * w.inv);
+          invs[i] = (float)(s != 0.0 ? 1.0 / s : 1.0);
+        }
+        named_sync(1, kNVW * 32);
+        const double sc = (double)in_h / (double)out_h;
+        const double sup = 2.0 * (sc > 1.0 ? sc : 1.0);
+        // per source row y: weights of its live rows i0..i0+cnt-1 as an aligned 8-float vector
+        // (w[0..cnt) , w[7] = cnt); i0 is implied by the output-row-ordered walk
+        for (int y = tid; y < in_h; y += kNVW * 32) {
+          int i = (int)floor(((double)y - sup - 0.5) / sc - 0.5);
+          if (i < 0) i = 0;
+          if (i > out_h) i = out_h;
+          while (i > 0 && y1t[i - 1] > y) --i;
+          while (i < out_h && y1t[i] <= y) ++i;
+          float wv[8] = {0.f, 0.f, 0.f, 0.f, 0.f, 0.f, 0.f, 0.f};
+          int cnt = 0;
+          for (int r = 0; r < kRing && i + r < out_h; ++r) {
+            const Win w = window_of(in_h, out_h, i + r);
+            if (w.x0 > y) break;
+            wv[r] = (float)keys_d(((double)y - w.c + 0.5) * w.inv) * invs[i + r];
+            ++cnt;
+          }
+          wv[7] = __int_as_float(cnt);
+          float4* dst = reinterpret_cast<float4*>(wrow + 8 * y);
+          dst[0] = make_float4(wv[0], wv[1], wv[2], wv[3]);
+          dst[1] = make_float4(wv[4], wv[5], wv[6], wv[7]);
+        }
+        named_sync(1, kNVW * 32);
+        cached_clip = k;
+      }
       for (; item < cend && item < my_b; ++item) {
         const int64_t local = item - pl.tile_offset;
-        const int f = (int)(local / nstrips), strip = (int)(local % nstrips);
-        const int j0 = strip * ws, jn = min(ws, pl.out_w - j0);
-        const Win wa = window_of(pl.in_w, pl.out_w, j0);
-        const Win wb = window_of(pl.in_w, pl.out_w, j0 + jn - 1);
-        const int b0 = (3 * wa.x0) & ~15;
-        int b1 = (3 * wb.x1 + 15) & ~15;
-        const int nbytes = b1 - b0;
-        const uint8_t* src = frames + coff + (int64_t)f * pl.in_h * pitch + b0;
-        for (int y = 0; y < pl.in_h; ++y) {
-          mbar_wait(&empty[slot], phase ^ 1);
-          mbar_arrive_expect_tx(&full[slot], (uint32_t)nbytes);
-          tma_bulk_g2s(ring + (size_t)slot * Cfg::FPB, src + (int64_t)y * pitch, (uint32_t)nbytes, &full[slot]);
-          if (++slot == kSlots) { slot = 0; phase ^= 1; }
+        const Strip st = strip_of(pl, ws, (int)(local % nstrips));
+        const int px_lane = warp * kWarpPx + lane * 4;      // this lane's first pixel (relative to pa)
+        const bool vactive = px_lane < st.np;
+        float4* vdst_base = vbuf + px_lane;
+        Acc acc;
+#pragma unroll
+        for (int r = 0; r < kRing; ++r)
+#pragma unroll
+          for (int q = 0; q < 6; ++q) acc[r][q] = make_float2(0.f, 0.f);
+        int y = 0;
+        // software pipeline: the staged bytes and the weight vector of row y are loaded one row ahead
+        uint32_t n0 = 0, n1 = 0, n2 = 0;
+        float4 nwa = make_float4(0.f, 0.f, 0.f, 0.f), nwb = nwa;
+        auto load_row = [&](int yy) {
+          mbar_wait(&full[rslot], rphase);
+          const uint32_t* sp = reinterpret_cast<const uint32_t*>(stage + rslot * kWarpB) + lane * 3;
+          n0 = sp[0]; n1 = sp[1]; n2 = sp[2];
+          const float4* wp = reinterpret_cast<const float4*>(wrow + 8 * yy);
+          nwa = wp[0]; nwb = wp[1];
+        };
+        if (in_h > 0) load_row(0);
+        // Output row i lives in ring slot i % kRing.  Unrolling the output-row loop by kRing makes every
+        // slot index static: for row i = ib + U, consume the source rows up to its window end y1_i (the
+        // first live row of each of them is i), then retire slot U.
+        for (int ib = 0; ib < out_h; ib += kRing) {
+#define VP_ROW(U)                                                                               \
+          if (ib + U < out_h) {                                                                 \
+            const int yend = y1t[ib + U];                                                       \
+            for (; y < yend; ++y) {                                                             \
+              const uint32_t r0 = n0, r1 = n1, r2 = n2;                                         \
+              const float4 wa = nwa, wb = nwb;                                                  \
+              const uint32_t used = rslot;                                                      \
+              if (++rslot == kDepth) { rslot = 0; rphase ^= 1; }                                \
+              if (y + 1 < in_h) load_row(y + 1);                                                \
+              __syncwarp();                                                                     \
+              if (lane == 0) pr.issue(stage, full, used);                                       \
+              float2 fv[6];                                                                     \
+              fv[0] = make_float2((float)(r0 & 0xffu), (float)((r0 >> 8) & 0xffu));            \
+              fv[1] = make_float2((float)((r0 >> 16) & 0xffu), (float)(r0 >> 24));             \
+              fv[2] = make_float2((float)(r1 & 0xffu), (float)((r1 >> 8) & 0xffu));            \
+              fv[3] = make_float2((float)((r1 >> 16) & 0xffu), (float)(r1 >> 24));             \
+              fv[4] = make_float2((float)(r2 & 0xffu), (float)((r2 >> 8) & 0xffu));            \
+              fv[5] = make_float2((float)((r2 >> 16) & 0xffu), (float)(r2 >> 24));             \
+              const float w6[6] = {wa.x, wa.y, wa.z, wa.w, wb.x, wb.y};                         \
+              ring_row<U>(acc, __float_as_int(wb.w), w6, fv);                                   \
+            }                                                                                   \
+            const uint32_t vs = vrow % kCapR, vph = (vrow / kCapR) & 1;                         \
+            mbar_wait(&vempty[vs], vph ^ 1);                                                    \
+            retire_slot<U>(acc, vdst_base + vs * kRowPx, vactive);                              \
+            __syncwarp();                                                                       \
+            if (lane == 0) mbar_arrive(&vfull[vs]);                                             \
+            ++vrow;                                                                             \
+          }
+          static_assert(kRing == 6, "unroll below");
+          VP_ROW(0) VP_ROW(1) VP_ROW(2) VP_ROW(3) VP_ROW(4) VP_ROW(5)
+#undef VP_ROW
+        }
+        // the row prefetched beyond the last window (if any) and all rows below it keep the ring in step
+        if (y < in_h) {
+          const uint32_t used = rslot;
+          if (++rslot == kDepth) { rslot = 0; rphase ^= 1; }
+          __syncwarp();
+          if (lane == 0) pr.issue(stage, full, used);
+          ++y;
+        }
+        // source rows below the last window (none for the supported ratios) keep the ring in step
+        for (; y < in_h; ++y) {
+          mbar_wait(&full[rslot], rphase);
+          __syncwarp();
+          if (lane == 0) pr.issue(stage, full, rslot);
+          if (++rslot == kDepth) { rslot = 0; rphase ^= 1; }
         }
       }
     }
     return;
   }
 
-  // ------------------------------------------------------------ consumers
-  const int NC = Cfg::NC;
+  // ============================================================ H warps: horizontal pass + store
+  asm volatile("setmaxnreg.dec.sync.aligned.u32 104;\n" ::: "memory");
+  const int ht = tid - kNVW * 32;       // 0..127
   const int p = kp.p, m = kp.m, tp = kp.tp, B = m * p;
-  uint32_t slot = 0, phase = 0;
-  int cached_clip = -1, cached_strip = -1;
-  float hw[Cfg::HREG ? Cfg::UPT * Cfg::LHM : 1];
-  int h_x[Cfg::UPT], h_c[Cfg::UPT], h_j[Cfg::UPT];
+  uint32_t vrow = 0;
   int64_t item = my_a;
   while (item < my_b) {
     const int k = find_clip_f(plans, n, item);
     const vp_clip_plan pl = plans[k];
     const int64_t cend = pl.tile_offset + pl.tile_count;
-    const int64_t coff = clip_off[k], pitch = pitch_arr[k];
-    if (!clip_is_mine(pl, VARIANT, coff, pitch)) {
+    if (!clip_is_mine(pl, VARIANT, clip_off[k], pitch_arr[k])) {
       item = cend;
       continue;
     }
     void* pv = pl.is_image ? pv_img : pv_vid;
     const int64_t cap = pl.is_image ? img_cap : vid_cap;
     const bool writable = pv != nullptr && pl.patch_offset + (int64_t)pl.grid_t * pl.grid_h * pl.grid_w <= cap;
-    const int ws = fast_strip_width(pl.in_w, pl.out_w, VARIANT);
+    const int ws = fast_strip_width(pl.in_w, pl.out_w);
     const int nstrips = (pl.out_w + ws - 1) / ws;
-    const int in_h = pl.in_h, out_h = pl.out_h;
-
-    if (k != cached_clip) {
-      // ---- vertical tables for this clip (K2), consumers only ----
-      named_sync(1, NC);
-      // A: 1/sum of each output row's weights (f32), aliased in vbuf
-      float* invs = vbuf;
-      for (int i = tid; i < out_h; i += NC) {
-        const Win w = window_of(in_h, out_h, i);
-        double s = 0.0;
-        for (int y = w.x0; y < w.x1; ++y) s += keys_d(((double)y - w.c + 0.5) * w.inv);
-        invs[i] = (float)(s != 0.0 ? 1.0 / s : 1.0);
-      }
-      // B: per source row: first live output row ia, live count, retiring count
-      const double sc = (double)in_h / (double)out_h;
-      const double sup = 2.0 * (sc > 1.0 ? sc : 1.0);
-      for (int y = tid; y < in_h; y += NC) {
-        // first i with x1_i > y: x1_i = int((i+0.5)s + sup + 0.5); estimate then correct
-        int i = (int)floor(((double)y - sup - 0.5) / sc - 0.5);
-        if (i < 0) i = 0;
-        while (i > 0 && window_of(in_h, out_h, i - 1).x1 > y) --i;
-        while (i < out_h && window_of(in_h, out_h, i).x1 <= y) ++i;
-        int cnt = 0, nret = 0;
-        for (int r = 0; r < kRing && i + r < out_h; ++r) {
-          const Win w = window_of(in_h, out_h, i + r);
-          if (w.x0 > y) break;
-          ++cnt;
-          if (w.x1 - 1 == y) ++nret;
-        }
-        meta[y] = make_int2(cnt, (i << 8) | (cnt << 4) | nret);
-      }
-      named_sync(1, NC);
-      // C: exclusive scan of cnt over rows (single warp, serial over chunks of 32)
-      if (warp == 0) {
-        int carry = 0;
-        for (int y0 = 0; y0 < in_h; y0 += 32) {
-          const int y = y0 + (tid & 31);
-          int v = y < in_h ? meta[y].x : 0, x = v;
-#pragma unroll
-          for (int o = 1; o < 32; o <<= 1) {
-            int t = __shfl_up_sync(0xffffffffu, x, o);
-            if ((tid & 31) >= o) x += t;
-          }
-          if (y < in_h) meta[y].x = carry + x - v;
-          carry += __shfl_sync(0xffffffffu, x, 31);
-        }
-      }
-      named_sync(1, NC);
-      // D: weights
-      for (int y = tid; y < in_h; y += NC) {
-        const int2 me = meta[y];
-        const int i0 = me.y >> 8, cnt = (me.y >> 4) & 15;
-        for (int r = 0; r < cnt; ++r) {
-          const Win w = window_of(in_h, out_h, i0 + r);
-          wl[me.x + r] = (float)keys_d(((double)y - w.c + 0.5) * w.inv) * invs[i0 + r];
-        }
-      }
-      named_sync(1, NC);
-      for (int i = tid; i < kCapR * Cfg::FPF; i += NC) vbuf[i] = 0.f;
-      cached_clip = k;
-      cached_strip = -1;
-    }
-
+    const int out_h = pl.out_h;
     for (; item < cend && item < my_b; ++item) {
       const int64_t local = item - pl.tile_offset;
-      const int f = (int)(local / nstrips), strip = (int)(local % nstrips);
-      const int j0 = strip * ws, jn = min(ws, pl.out_w - j0);
-      const Win wa = window_of(pl.in_w, pl.out_w, j0);
-      const Win wb = window_of(pl.in_w, pl.out_w, j0 + jn - 1);
-      const int b0 = (3 * wa.x0) & ~15;
-      const int nbytes = ((3 * wb.x1 + 15) & ~15) - b0;
-      if (strip != cached_strip) {
-        // ---- horizontal weights of this strip ----
-        named_sync(1, NC);
-        for (int jj = tid; jj < jn; jj += NC) {
-          const Win w = window_of(pl.in_w, pl.out_w, j0 + jj);
-          double s = 0.0, ww[Cfg::LHM];
-#pragma unroll 1
-          for (int l = 0; l < Cfg::LHM; ++l) {
-            ww[l] = (w.x0 + l < w.x1) ? keys_d(((double)(w.x0 + l) - w.c + 0.5) * w.inv) : 0.0;
-            s += ww[l];
-          }
-          const double r = s != 0.0 ? 1.0 / s : 1.0;
-#pragma unroll 1
-          for (int l = 0; l < Cfg::LHM; ++l) wh[jj * Cfg::LHM + l] = (float)(ww[l] * r);
-          hx[jj] = 3 * w.x0 - b0;                  // float index of (x0, channel 0) in a V row
-        }
-        named_sync(1, NC);
-        for (int u = 0; u < Cfg::UPT; ++u) {
-          const int unit = tid + u * NC;           // unit = c * jn + jj (consecutive threads -> consecutive px)
-          const int c = unit / jn, jj = unit - c * jn;
-          h_c[u] = c < 3 ? c : -1;
-          h_j[u] = jj;
-          h_x[u] = c < 3 ? hx[jj] + c : 0;
-          if (Cfg::HREG) {
-#pragma unroll
-            for (int l = 0; l < Cfg::LHM; ++l) hw[u * Cfg::LHM + l] = c < 3 ? wh[jj * Cfg::LHM + l] : 0.f;
-          }
-        }
-        cached_strip = strip;
+      const int f = (int)(local / nstrips);
+      const Strip st = strip_of(pl, ws, (int)(local % nstrips));
+      // ---- horizontal weights of this strip: layout [col pair][tap][2] ----
+      named_sync(2, kNHW * 32);
+      for (int jj = ht; jj < st.jn; jj += kNHW * 32) {
+        const Win w = window_of(pl.in_w, pl.out_w, st.j0 + jj);
+        double s = 0.0;
+        for (int x = w.x0; x < w.x1; ++x) s += keys_d(((double)x - w.c + 0.5) * w.inv);
+        const double r = s != 0.0 ? 1.0 / s : 1.0;
+        for (int l = 0; l < LHM; ++l)
+          wh[((jj >> 1) * LHM + l) * 2 + (jj & 1)] =
+              (w.x0 + l < w.x1) ? (float)(keys_d(((double)(w.x0 + l) - w.c + 0.5) * w.inv) * r) : 0.f;
+        hx[jj] = w.x0 - st.pa;                      // first tap pixel relative to the footprint start
       }
-      // slots filled by frame f (O7): f itself, and tp*gt-1 .. n for the last frame
-      const int n_fr = pl.n_frames;
-      const int last_slot = (f == n_fr - 1) ? pl.grid_t * tp - 1 : f;
-      const int gh = pl.grid_h, gw = pl.grid_w;
-
-      unsigned long long acc[16];
+      named_sync(2, kNHW * 32);
+      const int npairs = st.jn >> 1;                 // jn is even (multiple of the even factor p*m)
+      const bool hact = ht < npairs;
+      const int ja = 2 * ht;
+      const int xa = hact ? hx[ja] : 0, xb = hact ? hx[ja + 1] : 0;
+      float hw[Cfg::HREG ? 2 * LHM : 1];
+      if (Cfg::HREG) {
 #pragma unroll
-      for (int r = 0; r < 16; ++r) acc[r] = 0ull;
-      const int lane_f = tid * 4;                   // this lane's float index within a V row
-      const bool vactive = lane_f < nbytes;
-      int retired = 0, done = 0;
-
-      auto hpass = [&](int rows_to) {
-        // rows [done, rows_to) are in vbuf (row i at slot i & (kCapR-1))
-        named_sync(1, NC);
-        if (writable) {
-          for (int i = done; i < rows_to; ++i) {
-            const float* vrow = vbuf + (i & (kCapR - 1)) * Cfg::FPF;
-            const int hb = i / B, il = i - hb * B, mh = il / p, py = il - mh * p;
-#pragma unroll
-            for (int u = 0; u < Cfg::UPT; ++u) {
-              const int c = h_c[u];
-              if (c < 0) continue;
-              const float* vp_ = vrow + h_x[u];
-              float a = 0.f;
-              if (Cfg::HREG) {
-#pragma unroll
-                for (int l = 0; l < Cfg::LHM; ++l) a = fmaf(hw[u * Cfg::LHM + l], vp_[3 * l], a);
-              } else {
-                const float* wr = wh + h_j[u] * Cfg::LHM;
-#pragma unroll 8
-                for (int l = 0; l < Cfg::LHM; ++l) a = fmaf(wr[l], vp_[3 * l], a);
-              }
-              a = fminf(fmaxf(a, 0.f), 255.f);                            // C12
-              const float x = fmaf(a, kp.scale[c], kp.bias[c]);            // O6
-              const int j = j0 + h_j[u];
-              const int wbk = j / B, jl = j - wbk * B, mw = jl / p, px = jl - mw * p;
-              for (int sl = f; sl <= last_slot; ++sl) {
-                const int g = sl / tp, ti = sl - g * tp;
-                const int64_t row = pl.patch_offset + (((int64_t)g * (gh / m) + hb) * (gw / m) + wbk) * m * m +
-                                    mh * m + mw;
-                const int64_t q = ((int64_t)(c * tp + ti) * p + py) * p + px;
-                if (kF32) reinterpret_cast<float*>(pv)[row * kp.D + q] = x;
-                else reinterpret_cast<__nv_bfloat16*>(pv)[row * kp.D + q] = __float2bfloat16_rn(x);
-              }
-            }
-          }
+        for (int l = 0; l < LHM; ++l) {
+          hw[2 * l] = hact ? wh[(ht * LHM + l) * 2] : 0.f;
+          hw[2 * l + 1] = hact ? wh[(ht * LHM + l) * 2 + 1] : 0.f;
         }
-        done = rows_to;
-        named_sync(1, NC);
-      };
+      }
+      // column part of the output element index (O8): (wb*m^2 + mw)*D + px  (channel part added per c)
+      int colpart;
+      {
+        const int j = st.j0 + ja, wbk = j / B, jl = j - wbk * B, mw = jl / p, px = jl - mw * p;
+        colpart = (wbk * m * m + mw) * kp.D + px;
+      }
+      const int cstride = tp * p * p;
+      const int last_slot = (f == pl.n_frames - 1) ? pl.grid_t * tp - 1 : f;   // O7: frame n-1 fills pads
+      const int gh = pl.grid_h, gw = pl.grid_w;
+      const int g0 = f / tp, ti0 = f - g0 * tp;
+      const int64_t group_stride = (int64_t)(gh / m) * (gw / m) * m * m * kp.D;
+      const int64_t base0 = pl.patch_offset * (int64_t)kp.D + (int64_t)g0 * group_stride + (int64_t)ti0 * p * p;
+      const int nslots = last_slot - f + 1;
+      const int64_t hb_stride = (int64_t)(gw / m) * m * m * kp.D;
+      int r_hb = 0, r_mh = 0, r_py = 0;              // counters of the next row to emit
 
-      for (int y = 0; y < in_h; ++y) {
-        mbar_wait(&full[slot], phase);
-        unsigned long long f01 = 0ull, f23 = 0ull;
-        if (vactive) {
-          const uint32_t raw = *reinterpret_cast<const uint32_t*>(ring + (size_t)slot * Cfg::FPB + lane_f);
-          f01 = pack2((float)(raw & 0xffu), (float)((raw >> 8) & 0xffu));
-          f23 = pack2((float)((raw >> 16) & 0xffu), (float)(raw >> 24));
+      for (int i = 0; i < out_h; i += 2) {
+        const bool two = i + 1 < out_h;
+        const uint32_t s0 = vrow % kCapR, ph0 = (vrow / kCapR) & 1;
+        const uint32_t s1 = (vrow + 1) % kCapR, ph1 = ((vrow + 1) / kCapR) & 1;
+        mbar_wait(&vfull[s0], ph0);
+        if (two) mbar_wait(&vfull[s1], ph1);
+        const int64_t rp0 = base0 + r_hb * hb_stride + (int64_t)(r_mh * m) * kp.D + r_py * p;
+        if (++r_py == p) { r_py = 0; if (++r_mh == m) { r_mh = 0; ++r_hb; } }
+        const int64_t rp1 = base0 + r_hb * hb_stride + (int64_t)(r_mh * m) * kp.D + r_py * p;
+        if (two) { if (++r_py == p) { r_py = 0; if (++r_mh == m) { r_mh = 0; ++r_hb; } } }
+        if (writable && hact) {
+          const float4* v0 = vbuf + s0 * kRowPx;
+          const float4* v1 = vbuf + (two ? s1 : s0) * kRowPx;
+          // accumulators per (column, row): RG as a float2 (FFMA2 on the LDS.128 result's .xy pair, no
+          // repacking) and B as a float
+          float2 rg00 = make_float2(0.f, 0.f), rg01 = rg00, rg10 = rg00, rg11 = rg00;  // [col a/b][row 0/1]
+          float b00 = 0.f, b01 = 0.f, b10 = 0.f, b11 = 0.f;
+          const float2* wr = reinterpret_cast<const float2*>(wh) + ht * LHM;
+#pragma unroll
+          for (int l = 0; l < LHM; ++l) {
+            float wa, wb;
+            if (Cfg::HREG) { wa = hw[2 * l]; wb = hw[2 * l + 1]; }
+            else { const float2 t = wr[l]; wa = t.x; wb = t.y; }
+            const float4 pa0 = v0[xa + l], pa1 = v1[xa + l];
+            const float4 pb0 = v0[xb + l], pb1 = v1[xb + l];
+            const float2 wwa = make_float2(wa, wa), wwb = make_float2(wb, wb);
+            rg00 = __ffma2_rn(wwa, make_float2(pa0.x, pa0.y), rg00);
+            rg01 = __ffma2_rn(wwa, make_float2(pa1.x, pa1.y), rg01);
+            rg10 = __ffma2_rn(wwb, make_float2(pb0.x, pb0.y), rg10);
+            rg11 = __ffma2_rn(wwb, make_float2(pb1.x, pb1.y), rg11);
+            b00 = fmaf(wa, pa0.z, b00);
+            b01 = fmaf(wa, pa1.z, b01);
+            b10 = fmaf(wb, pb0.z, b10);
+            b11 = fmaf(wb, pb1.z, b11);
+          }
+          // clamp (C12), normalise (O6): x = v*scale_c + bias_c; store (col ja, ja+1) pairs
+#define VP_EMIT(VA, VB, C)                                                                             \
+          {                                                                                           \
+            const float sc_ = kp.scale[C], bi_ = kp.bias[C];                                          \
+            store_slots<kF32>(pv, rp0 + colpart + C * cstride, fmaf(fminf(fmaxf(VA##0, 0.f), 255.f), sc_, bi_), \
+                              fmaf(fminf(fmaxf(VB##0, 0.f), 255.f), sc_, bi_), nslots, ti0, tp, p, group_stride); \
+            if (two)                                                                                  \
+              store_slots<kF32>(pv, rp1 + colpart + C * cstride, fmaf(fminf(fmaxf(VA##1, 0.f), 255.f), sc_, bi_), \
+                                fmaf(fminf(fmaxf(VB##1, 0.f), 255.f), sc_, bi_), nslots, ti0, tp, p, group_stride); \
+          }
+          const float r_a0 = rg00.x, r_a1 = rg01.x, r_b0 = rg10.x, r_b1 = rg11.x;
+          const float g_a0 = rg00.y, g_a1 = rg01.y, g_b0 = rg10.y, g_b1 = rg11.y;
+          const float b0_0 = b00, b0_1 = b01, b1_0 = b10, b1_1 = b11;
+          VP_EMIT(r_a, r_b, 0) VP_EMIT(g_a, g_b, 1) VP_EMIT(b0_, b1_, 2)
+#undef VP_EMIT
         }
         __syncwarp();
-        if ((tid & 31) == 0) mbar_arrive(&empty[slot]);
-        if (++slot == kSlots) { slot = 0; phase ^= 1; }
-        const int2 me = meta[y];
-        const int ia = me.y >> 8, cnt = (me.y >> 4) & 15, nret = me.y & 15;
-        ring_step(acc, ((ia & 7) << 4) | cnt, wl + me.x, f01, f23);
-        if (nret) {
-          ring_retire_dispatch(acc, ((ia & 7) << 2) | nret, vbuf, ia, Cfg::FPF, lane_f, vactive);
-          retired = ia + nret;
-          if (retired - done >= kQH) hpass(retired);
+        if (lane == 0) {
+          mbar_arrive(&vempty[s0]);
+          if (two) mbar_arrive(&vempty[s1]);
         }
+        vrow += two ? 2 : 1;
       }
-      if (retired > done) hpass(retired);
     }
   }
-  (void)misc;
 }
 
 int g_num_sms = 0;
-bool g_attr[2][2] = {{false, false}, {false, false}};
+bool g_attr[3][2] = {};
 
 template <int VARIANT, bool kF32>
 void launch_fast(const FKParams& kp, const vp_clip_plan* plans, int n, const uint8_t* frames, const int64_t* coff,
                  const int64_t* pitch, void* pi, int64_t icap, void* pvv, int64_t vcap, cudaStream_t s) {
-  using Cfg = FastCfg<VARIANT, kF32>;
+  using Cfg = FastCfg<VARIANT>;
   auto kern = resize_fast_kernel<VARIANT, kF32>;
   if (!g_attr[VARIANT][kF32]) {
     cudaFuncSetAttribute(kern, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)Cfg::SMEM);
     g_attr[VARIANT][kF32] = true;
   }
   int per_sm = 0;
-  cudaOccupancyMaxActiveBlocksPerMultiprocessor(&per_sm, kern, Cfg::NC + 32, Cfg::SMEM);
+  cudaOccupancyMaxActiveBlocksPerMultiprocessor(&per_sm, kern, kNT, Cfg::SMEM);
   if (per_sm < 1) per_sm = 1;
-  const int grid = g_num_sms * per_sm;
-  kern<<<grid, Cfg::NC + 32, Cfg::SMEM, s>>>(kp, plans, n, frames, coff, pitch, pi, icap, pvv, vcap);
+  kern<<<g_num_sms * per_sm, kNT, Cfg::SMEM, s>>>(kp, plans, n, frames, coff, pitch, pi, icap, pvv, vcap);
 }
 
 }  // namespace
 
-// Launch both fast variants (each skips clips that are not its own).
+// Launch the fast variants (each skips clips that are not its own).
 void launch_resize_fast(const vp_params* p, const vp_clip_plan* plans, int n, const uint8_t* frames,
                         const int64_t* coff, const int64_t* pitch, void* pi, int64_t icap, void* pvv, int64_t vcap,
                         cudaStream_t s) {
@@ -539,9 +620,11 @@ void launch_resize_fast(const vp_params* p, const vp_clip_plan* plans, int n, co
   }
   if (p->out_dtype == VP_OUT_F32) {
     launch_fast<KV_MILD, true>(kp, plans, n, frames, coff, pitch, pi, icap, pvv, vcap, s);
+    launch_fast<KV_MEDIUM, true>(kp, plans, n, frames, coff, pitch, pi, icap, pvv, vcap, s);
     launch_fast<KV_STRONG, true>(kp, plans, n, frames, coff, pitch, pi, icap, pvv, vcap, s);
   } else {
     launch_fast<KV_MILD, false>(kp, plans, n, frames, coff, pitch, pi, icap, pvv, vcap, s);
+    launch_fast<KV_MEDIUM, false>(kp, plans, n, frames, coff, pitch, pi, icap, pvv, vcap, s);
     launch_fast<KV_STRONG, false>(kp, plans, n, frames, coff, pitch, pi, icap, pvv, vcap, s);
   }
 }
