@@ -51,7 +51,7 @@ constexpr int kTotLen = VP_TOT_LEN;
 // are n_frames x n_strips for the fast variants, 0 for generic.  Integer / f64 exact.
 // ------------------------------------------------------------------------------------------
 enum { KV_MILD = 0, KV_MEDIUM = 1, KV_STRONG = 2, KV_GENERIC = 3 };
-constexpr int kRing = 6;          // vertical ring slots (max live output rows per source row)
+constexpr int kRing = 5;          // vertical ring slots: max live output rows per source row for in/out > 0.8
 constexpr int kInHMax = 1088;     // source rows supported by the fast kernel's per-row weight table
 constexpr int kWListMax = 6144;   // vertical weights (sum of window lengths) held in smem
 constexpr int kOutHMax = 2048;    // output rows (per-row tables; 12-bit index in the packed meta word)
@@ -90,8 +90,9 @@ __host__ __device__ __forceinline__ int fast_strip_width(int in_w, int out_w) {
 
 __host__ __device__ __forceinline__ int select_variant(int in_h, int in_w, int out_h, int out_w) {
   const double sv = (double)in_h / (double)out_h;
-  // live output rows per source row <= ceil(4 / s) for upscale, <= 5 for downscale: s >= 0.67 fits 6 slots
-  if (sv < 0.67 || in_h > kInHMax || out_h > kOutHMax) return KV_GENERIC;
+  // live output rows per source row <= floor(4/s)+1 for upscale (<= 5 iff s > 0.8) and <= 5 for downscale
+  // (trimmed windows; brute-forced in tests/test_oracle_pixels.py::test_live_rows_bound)
+  if (!(sv > 0.8) || in_h > kInHMax || out_h > kOutHMax) return KV_GENERIC;
   const double sh = (double)in_w / (double)out_w;
   if (sh < 0.6 || fast_strip_width(in_w, out_w) < 16) return KV_GENERIC;
   const int th = axis_max_taps(in_w, out_w);

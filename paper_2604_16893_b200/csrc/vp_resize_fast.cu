@@ -7,15 +7,15 @@
 //     source footprint and is its own TMA producer: lane 0 keeps kDepth rows of its slice in flight
 //     with cp.async.bulk (global -> smem, completion on a per-warp mbarrier); lane L converts its 4
 //     pixels (12 bytes, I2F.U8) once per source row and FMAs them (FFMA2) into the <= 8 output rows
-//     live at that row, held in a register ring acc[6].  Output row i lives in slot i % 6; the
-//     output-row loop is unrolled by 6 so every slot index is static (no dynamic register indexing,
+//     live at that row, held in a register ring acc[5].  Output row i lives in slot i % 5; the
+//     output-row loop is unrolled by 5 so every slot index is static (no dynamic register indexing,
 //     no accumulator shuffles), and each source row dispatches once on its live count.
 //   * 4 H warps (horizontal pass).  Retired rows arrive through a 4-row smem buffer, pixel-major
 //     (float4 = RGB + pad) with mbarrier hand-off; each H thread computes 2 adjacent output columns x
 //     2 rows x 3 channels (LDS.128 + FFMA2, horizontal weights in registers for MILD), clamps,
 //     normalises and stores bf16x2 / float2 straight into the HF patch layout, once per temporal slot
 //     the frame fills (O7) -- every output element is written exactly once.
-// Registers are rebalanced between the warpgroups with setmaxnreg (V holds the 72-register ring).
+// Registers are rebalanced between the warpgroups with setmaxnreg (V holds the 60-register ring).
 // Per-clip tables (cached across a CTA's consecutive items): per source row an aligned 8-float vector
 // of the weights of its live output rows + the live count (fp32 from f64); windows are trimmed of
 // exact-zero taps (identity axes become 1-tap copies).  Per item: the strip's horizontal weights.
@@ -140,29 +140,17 @@ __device__ __forceinline__ Strip strip_of(const vp_clip_plan& pl, int ws, int st
 // `slot` (= row & 7).
 typedef float2 Acc[kRing][6];
 
-template <int BASE, int CNT>
-__device__ __forceinline__ void ring_contrib(Acc& acc, const float* __restrict__ w, const float2 (&f)[6]) {
+// contributions of one source row to the live rows i..i+5, where row i sits in slot U (static).
+// Dense over the 6 ring slots: the weight vector holds 0 for rows that are not live, so the code is
+// straight-line FFMA2 with no per-row branch (a 0-weight FMA adds exactly 0).
+template <int U>
+__device__ __forceinline__ void ring_row(Acc& acc, const float (&w)[kRing], const float2 (&f)[6]) {
 #pragma unroll
-  for (int r = 0; r < CNT; ++r) {
-    const int slot = (BASE + r) % kRing;
-    const float wr = w[r];
-    const float2 ww = make_float2(wr, wr);
+  for (int r = 0; r < kRing; ++r) {
+    const int slot = (U + r) % kRing;
+    const float2 ww = make_float2(w[r], w[r]);
 #pragma unroll
     for (int q = 0; q < 6; ++q) acc[slot][q] = __ffma2_rn(ww, f[q], acc[slot][q]);
-  }
-}
-
-// contributions of one source row to the live rows i..i+cnt-1, where row i sits in slot U (static)
-template <int U>
-__device__ __forceinline__ void ring_row(Acc& acc, int cnt, const float* __restrict__ w, const float2 (&f)[6]) {
-  switch (cnt) {
-    case 1: ring_contrib<U, 1>(acc, w, f); break;
-    case 2: ring_contrib<U, 2>(acc, w, f); break;
-    case 3: ring_contrib<U, 3>(acc, w, f); break;
-    case 4: ring_contrib<U, 4>(acc, w, f); break;
-    case 5: ring_contrib<U, 5>(acc, w, f); break;
-    case 6: ring_contrib<U, 6>(acc, w, f); break;
-    default: break;
   }
 }
 
@@ -211,62 +199,53 @@ struct FastCfg {
 };
 
 // Per-V-warp TMA producer (lane 0): walks the CTA's item sequence and keeps its slice of kDepth rows
-// in flight.  issue() refills the slot of the row the warp has just finished reading.
-template <int VARIANT>
-struct Producer {
-  const vp_clip_plan* plans;
-  int n, w;
-  const uint8_t* frames;
-  const int64_t* clip_off;
-  const int64_t* pitch_arr;
-  int64_t item, my_b, cend;
-  int y, in_h, nbytes;
+// in flight.  issue() refills the slot of the row the warp has just finished reading.  The per-item
+// setup is a separate non-inlined function returning by value, so the per-row state stays in registers.
+struct ProdItem {
+  const uint8_t* src;   // this warp's slice of source row 0 of the item (nullptr: no more items)
   int64_t pitch;
-  const uint8_t* src;
-  bool live;
-
-  __device__ __noinline__ void open_item() {
-    while (item < my_b) {
-      const int k = find_clip_f(plans, n, item);
-      const vp_clip_plan pl = plans[k];
-      cend = pl.tile_offset + pl.tile_count;
-      const int64_t coff = clip_off[k];
-      pitch = pitch_arr[k];
-      if (!clip_is_mine(pl, VARIANT, coff, pitch)) {
-        item = cend;
-        continue;
-      }
-      const int ws = fast_strip_width(pl.in_w, pl.out_w);
-      const int nstrips = (pl.out_w + ws - 1) / ws;
-      const int64_t local = item - pl.tile_offset;
-      const int f = (int)(local / nstrips), strip = (int)(local % nstrips);
-      const Strip st = strip_of(pl, ws, strip);
-      const int px0 = st.pa + w * kWarpPx;                       // this warp's first pixel
-      const int pxn = min(kWarpPx, st.pa + st.np - px0);         // its pixels (may be <= 0)
-      // 16-B multiple, never past the 16-B rounded row end (pitch is a multiple of 16 >= 3*in_w)
-      nbytes = pxn > 0 ? min(kWarpB, (3 * (px0 + pxn) + 15) / 16 * 16 - 3 * px0) : 0;
-      src = frames + coff + (int64_t)f * pl.in_h * pitch + 3 * (int64_t)px0;
-      in_h = pl.in_h;
-      y = 0;
-      live = true;
-      return;
-    }
-    live = false;
-  }
-  __device__ __forceinline__ void issue(uint8_t* stage, uint64_t* full, uint32_t slot) {
-    if (!live) return;
-    if (nbytes > 0) {
-      mbar_arrive_expect_tx(&full[slot], (uint32_t)nbytes);
-      tma_bulk_g2s(stage + (size_t)slot * kWarpB, src + (int64_t)y * pitch, (uint32_t)nbytes, &full[slot]);
-    } else {
-      mbar_arrive(&full[slot]);                                   // empty slice: complete the phase
-    }
-    if (++y == in_h) {
-      ++item;
-      open_item();
-    }
-  }
+  int64_t item;         // item index of this slice
+  int in_h, nbytes;
 };
+
+template <int VARIANT>
+__device__ __noinline__ ProdItem producer_open(const vp_clip_plan* __restrict__ plans, int n, int w,
+                                               const uint8_t* __restrict__ frames,
+                                               const int64_t* __restrict__ clip_off,
+                                               const int64_t* __restrict__ pitch_arr, int64_t item, int64_t my_b) {
+  ProdItem r;
+  r.src = nullptr;
+  r.pitch = 0;
+  r.item = item;
+  r.in_h = 0;
+  r.nbytes = 0;
+  while (item < my_b) {
+    const int k = find_clip_f(plans, n, item);
+    const vp_clip_plan pl = plans[k];
+    const int64_t cend = pl.tile_offset + pl.tile_count;
+    const int64_t coff = clip_off[k], pitch = pitch_arr[k];
+    if (!clip_is_mine(pl, VARIANT, coff, pitch)) {
+      item = cend;
+      continue;
+    }
+    const int ws = fast_strip_width(pl.in_w, pl.out_w);
+    const int nstrips = (pl.out_w + ws - 1) / ws;
+    const int64_t local = item - pl.tile_offset;
+    const int f = (int)(local / nstrips), strip = (int)(local % nstrips);
+    const Strip st = strip_of(pl, ws, strip);
+    const int px0 = st.pa + w * kWarpPx;                       // this warp's first pixel
+    const int pxn = min(kWarpPx, st.pa + st.np - px0);         // its pixels (may be <= 0)
+    // 16-B multiple, never past the 16-B rounded row end (pitch is a multiple of 16 >= 3*in_w)
+    r.nbytes = pxn > 0 ? min(kWarpB, (3 * (px0 + pxn) + 15) / 16 * 16 - 3 * px0) : 0;
+    r.src = frames + coff + (int64_t)f * pl.in_h * pitch + 3 * (int64_t)px0;
+    r.pitch = pitch;
+    r.in_h = pl.in_h;
+    r.item = item;
+    return r;
+  }
+  r.item = item;
+  return r;
+}
 
 template <int VARIANT, bool kF32>
 __global__ void __launch_bounds__(kNT, 2)
@@ -316,13 +295,32 @@ resize_fast_kernel(FKParams kp, const vp_clip_plan* __restrict__ plans, int n, c
     uint32_t rslot = 0, rphase = 0;   // staging ring position of the next row to read
     uint32_t vrow = 0;                // running count of retired rows (vbuf slot = vrow % kCapR)
     int cached_clip = -1;
-    Producer<VARIANT> pr;
-    if (lane == 0) {
-      pr.plans = plans; pr.n = n; pr.w = warp; pr.frames = frames; pr.clip_off = clip_off;
-      pr.pitch_arr = pitch_arr; pr.item = my_a; pr.my_b = my_b;
-      pr.open_item();
-      for (uint32_t q = 0; q < kDepth; ++q) pr.issue(stage, full, q);     // prefill
-    }
+    // producer state (meaningful in lane 0 only): current slice source row pointer + rows left
+    ProdItem pit = {nullptr, 0, my_a, 0, 0};
+    const uint8_t* psrc = nullptr;
+    int prows = 0;
+    auto issue = [&](uint32_t slot) {
+      if (prows == 0) {
+        if (pit.src != nullptr || pit.item == my_a) {
+          pit = producer_open<VARIANT>(plans, n, warp, frames, clip_off, pitch_arr,
+                                       pit.src != nullptr ? pit.item + 1 : my_a, my_b);
+          if (pit.src == nullptr) pit.item = -1;       // exhausted
+          psrc = pit.src;
+          prows = pit.in_h;
+        }
+        if (prows == 0) return;
+      }
+      if (pit.nbytes > 0) {
+        mbar_arrive_expect_tx(&full[slot], (uint32_t)pit.nbytes);
+        tma_bulk_g2s(stage + (size_t)slot * kWarpB, psrc, (uint32_t)pit.nbytes, &full[slot]);
+      } else {
+        mbar_arrive(&full[slot]);                                   // empty slice: complete the phase
+      }
+      psrc += pit.pitch;
+      --prows;
+    };
+    if (lane == 0)
+      for (uint32_t q = 0; q < kDepth; ++q) issue(q);     // prefill
     int64_t item = my_a;
     while (item < my_b) {
       const int k = find_clip_f(plans, n, item);
@@ -410,7 +408,7 @@ resize_fast_kernel(FKParams kp, const vp_clip_plan* __restrict__ plans, int n, c
               if (++rslot == kDepth) { rslot = 0; rphase ^= 1; }                                \
               if (y + 1 < in_h) load_row(y + 1);                                                \
               __syncwarp();                                                                     \
-              if (lane == 0) pr.issue(stage, full, used);                                       \
+              if (lane == 0) issue(used);                                       \
               float2 fv[6];                                                                     \
               fv[0] = make_float2((float)(r0 & 0xffu), (float)((r0 >> 8) & 0xffu));            \
               fv[1] = make_float2((float)((r0 >> 16) & 0xffu), (float)(r0 >> 24));             \
@@ -418,8 +416,8 @@ resize_fast_kernel(FKParams kp, const vp_clip_plan* __restrict__ plans, int n, c
               fv[3] = make_float2((float)((r1 >> 16) & 0xffu), (float)(r1 >> 24));             \
               fv[4] = make_float2((float)(r2 & 0xffu), (float)((r2 >> 8) & 0xffu));            \
               fv[5] = make_float2((float)((r2 >> 16) & 0xffu), (float)(r2 >> 24));             \
-              const float w6[6] = {wa.x, wa.y, wa.z, wa.w, wb.x, wb.y};                         \
-              ring_row<U>(acc, __float_as_int(wb.w), w6, fv);                                   \
+              const float w5[kRing] = {wa.x, wa.y, wa.z, wa.w, wb.x};                           \
+              ring_row<U>(acc, w5, fv);                                                         \
             }                                                                                   \
             const uint32_t vs = vrow % kCapR, vph = (vrow / kCapR) & 1;                         \
             mbar_wait(&vempty[vs], vph ^ 1);                                                    \
@@ -428,8 +426,8 @@ resize_fast_kernel(FKParams kp, const vp_clip_plan* __restrict__ plans, int n, c
             if (lane == 0) mbar_arrive(&vfull[vs]);                                             \
             ++vrow;                                                                             \
           }
-          static_assert(kRing == 6, "unroll below");
-          VP_ROW(0) VP_ROW(1) VP_ROW(2) VP_ROW(3) VP_ROW(4) VP_ROW(5)
+          static_assert(kRing == 5, "unroll below");
+          VP_ROW(0) VP_ROW(1) VP_ROW(2) VP_ROW(3) VP_ROW(4)
 #undef VP_ROW
         }
         // the row prefetched beyond the last window (if any) and all rows below it keep the ring in step
@@ -437,15 +435,16 @@ resize_fast_kernel(FKParams kp, const vp_clip_plan* __restrict__ plans, int n, c
           const uint32_t used = rslot;
           if (++rslot == kDepth) { rslot = 0; rphase ^= 1; }
           __syncwarp();
-          if (lane == 0) pr.issue(stage, full, used);
+          if (lane == 0) issue(used);
           ++y;
         }
         // source rows below the last window (none for the supported ratios) keep the ring in step
         for (; y < in_h; ++y) {
           mbar_wait(&full[rslot], rphase);
           __syncwarp();
-          if (lane == 0) pr.issue(stage, full, rslot);
+          const uint32_t used = rslot;
           if (++rslot == kDepth) { rslot = 0; rphase ^= 1; }
+          if (lane == 0) issue(used);
         }
       }
     }
@@ -553,20 +552,54 @@ resize_fast_kernel(FKParams kp, const vp_clip_plan* __restrict__ plans, int n, c
             b11 = fmaf(wb, pb1.z, b11);
           }
           // clamp (C12), normalise (O6): x = v*scale_c + bias_c; store (col ja, ja+1) pairs
-#define VP_EMIT(VA, VB, C)                                                                             \
-          {                                                                                           \
-            const float sc_ = kp.scale[C], bi_ = kp.bias[C];                                          \
-            store_slots<kF32>(pv, rp0 + colpart + C * cstride, fmaf(fminf(fmaxf(VA##0, 0.f), 255.f), sc_, bi_), \
-                              fmaf(fminf(fmaxf(VB##0, 0.f), 255.f), sc_, bi_), nslots, ti0, tp, p, group_stride); \
-            if (two)                                                                                  \
-              store_slots<kF32>(pv, rp1 + colpart + C * cstride, fmaf(fminf(fmaxf(VA##1, 0.f), 255.f), sc_, bi_), \
-                                fmaf(fminf(fmaxf(VB##1, 0.f), 255.f), sc_, bi_), nslots, ti0, tp, p, group_stride); \
+          const float xr0a = fmaf(fminf(fmaxf(rg00.x, 0.f), 255.f), kp.scale[0], kp.bias[0]);
+          const float xr0b = fmaf(fminf(fmaxf(rg10.x, 0.f), 255.f), kp.scale[0], kp.bias[0]);
+          const float xg0a = fmaf(fminf(fmaxf(rg00.y, 0.f), 255.f), kp.scale[1], kp.bias[1]);
+          const float xg0b = fmaf(fminf(fmaxf(rg10.y, 0.f), 255.f), kp.scale[1], kp.bias[1]);
+          const float xb0a = fmaf(fminf(fmaxf(b00, 0.f), 255.f), kp.scale[2], kp.bias[2]);
+          const float xb0b = fmaf(fminf(fmaxf(b10, 0.f), 255.f), kp.scale[2], kp.bias[2]);
+          const float xr1a = fmaf(fminf(fmaxf(rg01.x, 0.f), 255.f), kp.scale[0], kp.bias[0]);
+          const float xr1b = fmaf(fminf(fmaxf(rg11.x, 0.f), 255.f), kp.scale[0], kp.bias[0]);
+          const float xg1a = fmaf(fminf(fmaxf(rg01.y, 0.f), 255.f), kp.scale[1], kp.bias[1]);
+          const float xg1b = fmaf(fminf(fmaxf(rg11.y, 0.f), 255.f), kp.scale[1], kp.bias[1]);
+          const float xb1a = fmaf(fminf(fmaxf(b01, 0.f), 255.f), kp.scale[2], kp.bias[2]);
+          const float xb1b = fmaf(fminf(fmaxf(b11, 0.f), 255.f), kp.scale[2], kp.bias[2]);
+          if (nslots == 1) {
+            // common case: one temporal slot -> 3 (or 6) stores at constant channel offsets from a row pointer
+            if (kF32) {
+              float* q0 = reinterpret_cast<float*>(pv) + rp0 + colpart;
+              *reinterpret_cast<float2*>(q0) = make_float2(xr0a, xr0b);
+              *reinterpret_cast<float2*>(q0 + cstride) = make_float2(xg0a, xg0b);
+              *reinterpret_cast<float2*>(q0 + 2 * cstride) = make_float2(xb0a, xb0b);
+              if (two) {
+                float* q1 = reinterpret_cast<float*>(pv) + rp1 + colpart;
+                *reinterpret_cast<float2*>(q1) = make_float2(xr1a, xr1b);
+                *reinterpret_cast<float2*>(q1 + cstride) = make_float2(xg1a, xg1b);
+                *reinterpret_cast<float2*>(q1 + 2 * cstride) = make_float2(xb1a, xb1b);
+              }
+            } else {
+              __nv_bfloat16* q0 = reinterpret_cast<__nv_bfloat16*>(pv) + rp0 + colpart;
+              *reinterpret_cast<__nv_bfloat162*>(q0) = __floats2bfloat162_rn(xr0a, xr0b);
+              *reinterpret_cast<__nv_bfloat162*>(q0 + cstride) = __floats2bfloat162_rn(xg0a, xg0b);
+              *reinterpret_cast<__nv_bfloat162*>(q0 + 2 * cstride) = __floats2bfloat162_rn(xb0a, xb0b);
+              if (two) {
+                __nv_bfloat16* q1 = reinterpret_cast<__nv_bfloat16*>(pv) + rp1 + colpart;
+                *reinterpret_cast<__nv_bfloat162*>(q1) = __floats2bfloat162_rn(xr1a, xr1b);
+                *reinterpret_cast<__nv_bfloat162*>(q1 + cstride) = __floats2bfloat162_rn(xg1a, xg1b);
+                *reinterpret_cast<__nv_bfloat162*>(q1 + 2 * cstride) = __floats2bfloat162_rn(xb1a, xb1b);
+              }
+            }
+          } else {
+            // frame n-1 of a clip also fills the temporal pad slots (O7), images fill tp slots
+            store_slots<kF32>(pv, rp0 + colpart, xr0a, xr0b, nslots, ti0, tp, p, group_stride);
+            store_slots<kF32>(pv, rp0 + colpart + cstride, xg0a, xg0b, nslots, ti0, tp, p, group_stride);
+            store_slots<kF32>(pv, rp0 + colpart + 2 * cstride, xb0a, xb0b, nslots, ti0, tp, p, group_stride);
+            if (two) {
+              store_slots<kF32>(pv, rp1 + colpart, xr1a, xr1b, nslots, ti0, tp, p, group_stride);
+              store_slots<kF32>(pv, rp1 + colpart + cstride, xg1a, xg1b, nslots, ti0, tp, p, group_stride);
+              store_slots<kF32>(pv, rp1 + colpart + 2 * cstride, xb1a, xb1b, nslots, ti0, tp, p, group_stride);
+            }
           }
-          const float r_a0 = rg00.x, r_a1 = rg01.x, r_b0 = rg10.x, r_b1 = rg11.x;
-          const float g_a0 = rg00.y, g_a1 = rg01.y, g_b0 = rg10.y, g_b1 = rg11.y;
-          const float b0_0 = b00, b0_1 = b01, b1_0 = b10, b1_1 = b11;
-          VP_EMIT(r_a, r_b, 0) VP_EMIT(g_a, g_b, 1) VP_EMIT(b0_, b1_, 2)
-#undef VP_EMIT
         }
         __syncwarp();
         if (lane == 0) {

@@ -82,6 +82,17 @@ def test_random_shapes_and_pitches(seed):
     _full_compare(pre, clips, pitch_pad=rng.choice([0, 1, 5, 16]))
 
 
+@pytest.mark.parametrize("dtype", [1, 0])
+def test_mild_upscale_and_identity_edges(dtype):
+    """Ratios at the fast-path edges: in/out just above 0.8 (5-slot ring), identity, 1.0x-1.03x, and
+    just below 0.8 (generic kernel)."""
+    import paper_2604_16893_b200 as vp
+    pre = vp.VisualPreprocessor(image_max_pixels=1048576, video_max_pixels=1048576, max_frames=3, out_dtype=dtype)
+    clips = [I.image(27, 27), I.image(25, 25), I.image(1000, 1010), I.image(64, 96), I.clip(5, 2.0, 130, 100),
+             I.image(820, 1000)]
+    _full_compare(pre, clips)
+
+
 def test_cfg2_one_clip_full():
     """BASELINE cfg2 at full size, compared element by element (64 frames 720p -> 384x672)."""
     import paper_2604_16893_b200 as vp

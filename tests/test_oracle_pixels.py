@@ -148,3 +148,23 @@ def test_process_batch_end_to_end_small():
     assert res["video_grid_thw"].tolist() == [[4, 8, 8]]
     # identity resize + mean/std 0.5: values are exactly v/127.5 - 1
     assert np.max(np.abs(res["pixel_values_videos"] - O.patchify(fr / 127.5 - 1.0, 16, 2, 2))) < 1e-12
+
+
+def test_live_rows_bound():
+    """The fast kernel's 5-slot vertical ring assumes <= 5 output rows are live at any source row when
+    in/out > 0.8 (windows trimmed of exact-zero taps).  Brute force over many ratios."""
+    import random
+    rng = random.Random(0)
+    cases = [(720, 384), (1080, 128), (1024, 1024), (999, 1000), (801, 1000), (27, 32), (1080, 1088)]
+    for _ in range(1500):
+        out = rng.randint(16, 900)
+        inn = max(1, int(round(out * rng.uniform(0.801, 10.0))))
+        cases.append((inn, out))
+    for inn, out in cases:
+        if inn / out <= 0.8:
+            continue
+        live = np.zeros(inn, dtype=int)
+        for x0, w in O.aa_weights(inn, out):
+            nz = np.nonzero(w)[0]
+            live[x0 + nz[0]: x0 + nz[-1] + 1] += 1
+        assert live.max() <= 5, (inn, out)
