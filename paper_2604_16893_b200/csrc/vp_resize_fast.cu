@@ -29,7 +29,7 @@ namespace {
 constexpr int kNVW = 4;                   // V warps
 constexpr int kNHW = 4;                   // H warps
 constexpr int kNT = (kNVW + kNHW) * 32;   // 256 threads
-constexpr int kDepth = 8;                 // source rows in flight per V warp
+constexpr int kDepth = 12;                // source rows in flight per V warp (refilled in groups of 4)
 constexpr int kWarpPx = 128;              // pixels per V warp slice (32 lanes x 4 px)
 constexpr int kWarpB = 3 * kWarpPx;       // 384 bytes
 constexpr int kCapR = 4;                  // retired-row buffer rows (V -> H)
@@ -184,15 +184,13 @@ template <int VARIANT>
 struct FastCfg {
   static constexpr int LHM = VARIANT == KV_MILD ? 9 : (VARIANT == KV_MEDIUM ? 18 : 40);
   static constexpr bool HREG = false;                    // horizontal weights: one LDS.64 per tap (both columns)
-  // strips: 15 + (Ws-1)*fs + taps + 1 <= kFastPx with fs >= 4 for STRONG -> Ws <= 128
-  static constexpr int MAXWS = VARIANT == KV_STRONG ? 128 : kFastMaxWs;
+  static constexpr int MAXWS = kFastMaxWs;
   static constexpr size_t OFF_STG = 0;                                                   // V staging
   static constexpr size_t OFF_VBUF = OFF_STG + (size_t)kNVW * kDepth * kWarpB;          // retired rows
   static constexpr size_t OFF_WROW = OFF_VBUF + (size_t)kCapR * kRowPx * 16;
-  static constexpr size_t OFF_SCR = OFF_WROW + (size_t)kInHMax * 32;
-  static constexpr size_t OFF_Y1 = OFF_SCR + (size_t)kOutHMax * 4;
+  static constexpr size_t OFF_Y1 = OFF_WROW + (size_t)kInHMax * 32;
   static constexpr size_t OFF_WH = OFF_Y1 + (size_t)kOutHMax * 4;
-  static constexpr size_t OFF_HX = OFF_WH + (size_t)MAXWS * LHM * 4;
+  static constexpr size_t OFF_HX = OFF_WH + (size_t)kWhFloats * 4;
   static constexpr size_t OFF_BAR = (OFF_HX + (size_t)MAXWS * 4 + 15) & ~(size_t)15;
   static constexpr size_t SMEM = OFF_BAR + (kNVW * kDepth + 2 * kCapR) * 8;
   static_assert(OFF_VBUF % 16 == 0 && OFF_WROW % 16 == 0 && OFF_WH % 16 == 0, "align");
@@ -258,7 +256,6 @@ resize_fast_kernel(FKParams kp, const vp_clip_plan* __restrict__ plans, int n, c
   uint8_t* stage_all = smem + Cfg::OFF_STG;
   float4* vbuf = reinterpret_cast<float4*>(smem + Cfg::OFF_VBUF);
   float* wrow = reinterpret_cast<float*>(smem + Cfg::OFF_WROW);     // [kInHMax][8] vertical weights
-  float* vscratch = reinterpret_cast<float*>(smem + Cfg::OFF_SCR);  // [kOutHMax] table-build scratch
   int* y1t = reinterpret_cast<int*>(smem + Cfg::OFF_Y1);
   float* wh = reinterpret_cast<float*>(smem + Cfg::OFF_WH);
   int* hx = reinterpret_cast<int*>(smem + Cfg::OFF_HX);
@@ -267,7 +264,11 @@ resize_fast_kernel(FKParams kp, const vp_clip_plan* __restrict__ plans, int n, c
   uint64_t* vempty = vfull + kCapR;                                         // H -> V
 
   const int tid = threadIdx.x;
-  const int warp = tid >> 5, lane = tid & 31;
+  // warp index as a warp-uniform value and lane id from the special register (kept in registers, not
+  // re-derived from %tid inside the row loops)
+  const int warp = __shfl_sync(0xffffffffu, tid >> 5, 0);
+  int lane;
+  asm volatile("mov.u32 %0, %%laneid;" : "=r"(lane));
 
   // contiguous slice of the batch's fast-item space
   const int64_t it_begin = plans[0].tile_offset;
@@ -335,14 +336,15 @@ resize_fast_kernel(FKParams kp, const vp_clip_plan* __restrict__ plans, int n, c
       const int in_h = pl.in_h, out_h = pl.out_h;
       if (k != cached_clip) {
         // ---- vertical tables for this clip (K2), V warps only ----
-        float* invs = reinterpret_cast<float*>(vscratch);   // 1/sum scratch (out_h floats)
+        // 1/sum of output row i lives in the unused slots 6,7 of the 8-float row vectors (the ring reads 0..4)
+#define VP_INVS(i) wrow[8 * ((i) >> 1) + 6 + ((i) & 1)]
         named_sync(1, kNVW * 32);
         for (int i = tid; i < out_h; i += kNVW * 32) {
           const Win w = window_of(in_h, out_h, i);
           y1t[i] = w.x1;
           double s = 0.0;
           for (int y = w.x0; y < w.x1; ++y) s += keys_d(((double)y - w.c + 0.5) * w.inv);
-          invs[i] = (float)(s != 0.0 ? 1.0 / s : 1.0);
+          VP_INVS(i) = (float)(s != 0.0 ? 1.0 / s : 1.0);
         }
         named_sync(1, kNVW * 32);
         const double sc = (double)in_h / (double)out_h;
@@ -360,15 +362,16 @@ resize_fast_kernel(FKParams kp, const vp_clip_plan* __restrict__ plans, int n, c
           for (int r = 0; r < kRing && i + r < out_h; ++r) {
             const Win w = window_of(in_h, out_h, i + r);
             if (w.x0 > y) break;
-            wv[r] = (float)keys_d(((double)y - w.c + 0.5) * w.inv) * invs[i + r];
+            wv[r] = (float)keys_d(((double)y - w.c + 0.5) * w.inv) * VP_INVS(i + r);
             ++cnt;
           }
-          wv[7] = __int_as_float(cnt);
+          (void)cnt;
           float4* dst = reinterpret_cast<float4*>(wrow + 8 * y);
           dst[0] = make_float4(wv[0], wv[1], wv[2], wv[3]);
-          dst[1] = make_float4(wv[4], wv[5], wv[6], wv[7]);
+          wrow[8 * y + 4] = wv[4];                       // slots 5..7: row-window scratch (VP_INVS)
         }
         named_sync(1, kNVW * 32);
+#undef VP_INVS
         cached_clip = k;
       }
       for (; item < cend && item < my_b; ++item) {
@@ -407,8 +410,10 @@ resize_fast_kernel(FKParams kp, const vp_clip_plan* __restrict__ plans, int n, c
               const uint32_t used = rslot;                                                      \
               if (++rslot == kDepth) { rslot = 0; rphase ^= 1; }                                \
               if (y + 1 < in_h) load_row(y + 1);                                                \
-              __syncwarp();                                                                     \
-              if (lane == 0) issue(used);                                       \
+              if ((used & 3) == 3) {                                                            \
+                __syncwarp();                                                                   \
+                if (lane == 0) { issue(used - 3); issue(used - 2); issue(used - 1); issue(used); } \
+              }                                                                                 \
               float2 fv[6];                                                                     \
               fv[0] = make_float2((float)(r0 & 0xffu), (float)((r0 >> 8) & 0xffu));            \
               fv[1] = make_float2((float)((r0 >> 16) & 0xffu), (float)(r0 >> 24));             \
@@ -434,8 +439,10 @@ resize_fast_kernel(FKParams kp, const vp_clip_plan* __restrict__ plans, int n, c
         if (y < in_h) {
           const uint32_t used = rslot;
           if (++rslot == kDepth) { rslot = 0; rphase ^= 1; }
-          __syncwarp();
-          if (lane == 0) issue(used);
+          if ((used & 3) == 3) {
+            __syncwarp();
+            if (lane == 0) { issue(used - 3); issue(used - 2); issue(used - 1); issue(used); }
+          }
           ++y;
         }
         // source rows below the last window (none for the supported ratios) keep the ring in step
@@ -444,7 +451,10 @@ resize_fast_kernel(FKParams kp, const vp_clip_plan* __restrict__ plans, int n, c
           __syncwarp();
           const uint32_t used = rslot;
           if (++rslot == kDepth) { rslot = 0; rphase ^= 1; }
-          if (lane == 0) issue(used);
+          if ((used & 3) == 3) {
+            __syncwarp();
+            if (lane == 0) { issue(used - 3); issue(used - 2); issue(used - 1); issue(used); }
+          }
         }
       }
     }
