@@ -57,7 +57,7 @@ constexpr int kWListMax = 6144;   // vertical weights (sum of window lengths) he
 constexpr int kOutHMax = 2048;    // output rows (per-row tables; 12-bit index in the packed meta word)
 constexpr int kFastPx = 512;      // source footprint pixels per row (4 V warps x 32 lanes x 4 px)
 constexpr int kFastMaxWs = 256;   // strip width bound: column pairs <= 128 H threads
-constexpr int kWhFloats = 2304;   // horizontal weight table (strip columns x taps) in smem
+constexpr int kWhFloats = 3072;   // horizontal weight table (strip columns x union taps) in smem
 
 __host__ __device__ __forceinline__ int fast_lhm(int variant) {
   return variant == KV_MILD ? 9 : (variant == KV_MEDIUM ? 18 : 40);
@@ -77,8 +77,8 @@ __host__ __device__ __forceinline__ int axis_max_taps(int in, int out) {
 __host__ __device__ __forceinline__ int fast_strip_width(int in_w, int out_w) {
   const double s = (double)in_w / (double)out_w;
   const int taps = axis_max_taps(in_w, out_w);
-  const int lhm = taps <= 9 ? 9 : (taps <= 18 ? 18 : 40);        // = fast_lhm(variant)
-  const int wcap = (kWhFloats / lhm) & ~15;                        // the strip's weights fit kWhFloats
+  const int ul = taps <= 9 ? 11 : (taps <= 18 ? 23 : 51);         // union taps of a column pair (FastCfg::UL)
+  const int wcap = (kWhFloats / ul) & ~15;                         // the strip's weights fit kWhFloats
   int wmax = 0;
   for (int cand = 16; cand <= kFastMaxWs && cand <= wcap; cand += 16) {
     if (15.0 + (cand - 1) * s + taps + 1.0 <= (double)kFastPx) wmax = cand; else break;

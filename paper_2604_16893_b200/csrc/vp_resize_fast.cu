@@ -183,7 +183,8 @@ __device__ __forceinline__ void store_slots(void* pv, int64_t idx, float v0, flo
 template <int VARIANT>
 struct FastCfg {
   static constexpr int LHM = VARIANT == KV_MILD ? 9 : (VARIANT == KV_MEDIUM ? 18 : 40);
-  static constexpr bool HREG = false;                    // horizontal weights: one LDS.64 per tap (both columns)
+  // union of two adjacent columns' windows: LHM + the largest start shift between them (<= ceil(fs)+1)
+  static constexpr int UL = VARIANT == KV_MILD ? 11 : (VARIANT == KV_MEDIUM ? 23 : 51);
   static constexpr int MAXWS = kFastMaxWs;
   static constexpr size_t OFF_STG = 0;                                                   // V staging
   static constexpr size_t OFF_VBUF = OFF_STG + (size_t)kNVW * kDepth * kWarpB;          // retired rows
@@ -251,7 +252,7 @@ resize_fast_kernel(FKParams kp, const vp_clip_plan* __restrict__ plans, int n, c
                    const int64_t* __restrict__ clip_off, const int64_t* __restrict__ pitch_arr, void* pv_img,
                    int64_t img_cap, void* pv_vid, int64_t vid_cap) {
   using Cfg = FastCfg<VARIANT>;
-  constexpr int LHM = Cfg::LHM;
+  constexpr int UL = Cfg::UL;
   extern __shared__ __align__(128) unsigned char smem[];
   uint8_t* stage_all = smem + Cfg::OFF_STG;
   float4* vbuf = reinterpret_cast<float4*>(smem + Cfg::OFF_VBUF);
@@ -401,9 +402,12 @@ resize_fast_kernel(FKParams kp, const vp_clip_plan* __restrict__ plans, int n, c
         // slot index static: for row i = ib + U, consume the source rows up to its window end y1_i (the
         // first live row of each of them is i), then retire slot U.
         for (int ib = 0; ib < out_h; ib += kRing) {
+          int yends[kRing];                        // window ends of rows ib..ib+4, loaded once per group
+#pragma unroll
+          for (int u = 0; u < kRing; ++u) yends[u] = y1t[min(ib + u, out_h - 1)];
 #define VP_ROW(U)                                                                               \
           if (ib + U < out_h) {                                                                 \
-            const int yend = y1t[ib + U];                                                       \
+            const int yend = yends[U];                                                          \
             for (; y < yend; ++y) {                                                             \
               const uint32_t r0 = n0, r1 = n1, r2 = n2;                                         \
               const float4 wa = nwa, wb = nwb;                                                  \
@@ -485,31 +489,29 @@ resize_fast_kernel(FKParams kp, const vp_clip_plan* __restrict__ plans, int n, c
       const int64_t local = item - pl.tile_offset;
       const int f = (int)(local / nstrips);
       const Strip st = strip_of(pl, ws, (int)(local % nstrips));
-      // ---- horizontal weights of this strip: layout [col pair][tap][2] ----
+      // ---- horizontal weights of this strip: per column pair (ja, ja+1) the union of the two windows
+      //      starting at x0(ja), UL taps, layout [pair][u][2] (0 outside each column's window) ----
       named_sync(2, kNHW * 32);
-      for (int jj = ht; jj < st.jn; jj += kNHW * 32) {
-        const Win w = window_of(pl.in_w, pl.out_w, st.j0 + jj);
-        double s = 0.0;
-        for (int x = w.x0; x < w.x1; ++x) s += keys_d(((double)x - w.c + 0.5) * w.inv);
-        const double r = s != 0.0 ? 1.0 / s : 1.0;
-        for (int l = 0; l < LHM; ++l)
-          wh[((jj >> 1) * LHM + l) * 2 + (jj & 1)] =
-              (w.x0 + l < w.x1) ? (float)(keys_d(((double)(w.x0 + l) - w.c + 0.5) * w.inv) * r) : 0.f;
-        hx[jj] = w.x0 - st.pa;                      // first tap pixel relative to the footprint start
+      for (int cpi = ht; cpi < (st.jn >> 1); cpi += kNHW * 32) {
+        const Win w0 = window_of(pl.in_w, pl.out_w, st.j0 + 2 * cpi);
+        const Win w1 = window_of(pl.in_w, pl.out_w, st.j0 + 2 * cpi + 1);
+        double s0 = 0.0, s1 = 0.0;
+        for (int x = w0.x0; x < w0.x1; ++x) s0 += keys_d(((double)x - w0.c + 0.5) * w0.inv);
+        for (int x = w1.x0; x < w1.x1; ++x) s1 += keys_d(((double)x - w1.c + 0.5) * w1.inv);
+        const double r0 = s0 != 0.0 ? 1.0 / s0 : 1.0, r1 = s1 != 0.0 ? 1.0 / s1 : 1.0;
+        for (int u = 0; u < UL; ++u) {
+          const int x = w0.x0 + u;
+          wh[(cpi * UL + u) * 2] = (x < w0.x1) ? (float)(keys_d(((double)x - w0.c + 0.5) * w0.inv) * r0) : 0.f;
+          wh[(cpi * UL + u) * 2 + 1] =
+              (x >= w1.x0 && x < w1.x1) ? (float)(keys_d(((double)x - w1.c + 0.5) * w1.inv) * r1) : 0.f;
+        }
+        hx[cpi] = w0.x0 - st.pa;                      // union start relative to the footprint start
       }
       named_sync(2, kNHW * 32);
       const int npairs = st.jn >> 1;                 // jn is even (multiple of the even factor p*m)
       const bool hact = ht < npairs;
       const int ja = 2 * ht;
-      const int xa = hact ? hx[ja] : 0, xb = hact ? hx[ja + 1] : 0;
-      float hw[Cfg::HREG ? 2 * LHM : 1];
-      if (Cfg::HREG) {
-#pragma unroll
-        for (int l = 0; l < LHM; ++l) {
-          hw[2 * l] = hact ? wh[(ht * LHM + l) * 2] : 0.f;
-          hw[2 * l + 1] = hact ? wh[(ht * LHM + l) * 2 + 1] : 0.f;
-        }
-      }
+      const int xu = hact ? hx[ht] : 0;
       // column part of the output element index (O8): (wb*m^2 + mw)*D + px  (channel part added per c)
       int colpart;
       {
@@ -543,23 +545,21 @@ resize_fast_kernel(FKParams kp, const vp_clip_plan* __restrict__ plans, int n, c
           // repacking) and B as a float
           float2 rg00 = make_float2(0.f, 0.f), rg01 = rg00, rg10 = rg00, rg11 = rg00;  // [col a/b][row 0/1]
           float b00 = 0.f, b01 = 0.f, b10 = 0.f, b11 = 0.f;
-          const float2* wr = reinterpret_cast<const float2*>(wh) + ht * LHM;
+          const float2* wr = reinterpret_cast<const float2*>(wh) + ht * UL;
 #pragma unroll
-          for (int l = 0; l < LHM; ++l) {
-            float wa, wb;
-            if (Cfg::HREG) { wa = hw[2 * l]; wb = hw[2 * l + 1]; }
-            else { const float2 t = wr[l]; wa = t.x; wb = t.y; }
-            const float4 pa0 = v0[xa + l], pa1 = v1[xa + l];
-            const float4 pb0 = v0[xb + l], pb1 = v1[xb + l];
-            const float2 wwa = make_float2(wa, wa), wwb = make_float2(wb, wb);
-            rg00 = __ffma2_rn(wwa, make_float2(pa0.x, pa0.y), rg00);
-            rg01 = __ffma2_rn(wwa, make_float2(pa1.x, pa1.y), rg01);
-            rg10 = __ffma2_rn(wwb, make_float2(pb0.x, pb0.y), rg10);
-            rg11 = __ffma2_rn(wwb, make_float2(pb1.x, pb1.y), rg11);
-            b00 = fmaf(wa, pa0.z, b00);
-            b01 = fmaf(wa, pa1.z, b01);
-            b10 = fmaf(wb, pb0.z, b10);
-            b11 = fmaf(wb, pb1.z, b11);
+          for (int u = 0; u < UL; ++u) {
+            const float2 wp = wr[u];                           // (col a, col b) weights at pixel xu+u
+            const float4 q0 = v0[xu + u], q1 = v1[xu + u];     // rows i, i+1
+            const float2 wwa = make_float2(wp.x, wp.x), wwb = make_float2(wp.y, wp.y);
+            const float2 g0 = make_float2(q0.x, q0.y), g1 = make_float2(q1.x, q1.y);
+            rg00 = __ffma2_rn(wwa, g0, rg00);
+            rg01 = __ffma2_rn(wwa, g1, rg01);
+            rg10 = __ffma2_rn(wwb, g0, rg10);
+            rg11 = __ffma2_rn(wwb, g1, rg11);
+            b00 = fmaf(wp.x, q0.z, b00);
+            b01 = fmaf(wp.x, q1.z, b01);
+            b10 = fmaf(wp.y, q0.z, b10);
+            b11 = fmaf(wp.y, q1.z, b11);
           }
           // clamp (C12), normalise (O6): x = v*scale_c + bias_c; store (col ja, ja+1) pairs
           const float xr0a = fmaf(fminf(fmaxf(rg00.x, 0.f), 255.f), kp.scale[0], kp.bias[0]);

@@ -168,3 +168,24 @@ def test_live_rows_bound():
             nz = np.nonzero(w)[0]
             live[x0 + nz[0]: x0 + nz[-1] + 1] += 1
         assert live.max() <= 5, (inn, out)
+
+
+def test_column_pair_union_bound():
+    """The fast kernel's horizontal pass loads the union of two adjacent output columns' (trimmed) windows:
+    <= 11 / 23 / 51 pixels for the MILD / MEDIUM / STRONG tap classes (taps <= 9 / 18 / 40)."""
+    import math
+    import random
+    rng = random.Random(1)
+    limit = {0: 11, 1: 23, 2: 51}
+    for _ in range(1500):
+        out = rng.randint(16, 700)
+        inn = max(1, int(round(out * rng.uniform(0.81, 9.5))))
+        fs = max(inn / out, 1.0)
+        taps = 1 if inn == out else math.floor(4 * fs) + 2
+        var = 0 if taps <= 9 else (1 if taps <= 18 else 2)
+        ws = []
+        for x0, w in O.aa_weights(inn, out):
+            nz = np.nonzero(w)[0]
+            ws.append((x0 + nz[0], x0 + nz[-1] + 1))
+        for j in range(0, len(ws) - 1, 2):
+            assert ws[j + 1][1] - ws[j][0] <= limit[var], (inn, out, j)
