@@ -30,6 +30,8 @@ constexpr int kNVW = 4;                   // V warps
 constexpr int kNHW = 4;                   // H warps
 constexpr int kNT = (kNVW + kNHW) * 32;   // 256 threads
 constexpr int kDepth = 12;                // source rows in flight per V warp (refilled in groups of 4)
+constexpr int kGrp = 4;                   // rows per TMA group (one mbarrier phase per group)
+constexpr int kNGrp = kDepth / kGrp;
 constexpr int kWarpPx = 128;              // pixels per V warp slice (32 lanes x 4 px)
 constexpr int kWarpB = 3 * kWarpPx;       // 384 bytes
 constexpr int kCapR = 4;                  // retired-row buffer rows (V -> H)
@@ -51,6 +53,9 @@ __device__ __forceinline__ void mbar_arrive_expect_tx(uint64_t* bar, uint32_t by
   asm volatile("mbarrier.arrive.expect_tx.release.cta.shared::cta.b64 _, [%0], %1;" ::"r"(smem_u32(bar)),
                "r"(bytes)
                : "memory");
+}
+__device__ __forceinline__ void mbar_expect_tx(uint64_t* bar, uint32_t bytes) {
+  asm volatile("mbarrier.expect_tx.relaxed.cta.shared::cta.b64 [%0], %1;" ::"r"(smem_u32(bar)), "r"(bytes) : "memory");
 }
 __device__ __forceinline__ void mbar_arrive(uint64_t* bar) {
   asm volatile("mbarrier.arrive.release.cta.shared::cta.b64 _, [%0];" ::"r"(smem_u32(bar)) : "memory");
@@ -193,7 +198,7 @@ struct FastCfg {
   static constexpr size_t OFF_WH = OFF_Y1 + (size_t)kOutHMax * 4;
   static constexpr size_t OFF_HX = OFF_WH + (size_t)kWhFloats * 4;
   static constexpr size_t OFF_BAR = (OFF_HX + (size_t)MAXWS * 4 + 15) & ~(size_t)15;
-  static constexpr size_t SMEM = OFF_BAR + (kNVW * kDepth + 2 * kCapR) * 8;
+  static constexpr size_t SMEM = OFF_BAR + (kNVW * kNGrp + 2 * (kCapR / 2)) * 8;
   static_assert(OFF_VBUF % 16 == 0 && OFF_WROW % 16 == 0 && OFF_WH % 16 == 0, "align");
 };
 
@@ -261,8 +266,8 @@ resize_fast_kernel(FKParams kp, const vp_clip_plan* __restrict__ plans, int n, c
   float* wh = reinterpret_cast<float*>(smem + Cfg::OFF_WH);
   int* hx = reinterpret_cast<int*>(smem + Cfg::OFF_HX);
   uint64_t* full_all = reinterpret_cast<uint64_t*>(smem + Cfg::OFF_BAR);   // [kNVW][kDepth]
-  uint64_t* vfull = full_all + kNVW * kDepth;                               // retired rows: V -> H
-  uint64_t* vempty = vfull + kCapR;                                         // H -> V
+  uint64_t* vfull = full_all + kNVW * kNGrp;                                // retired row pairs: V -> H
+  uint64_t* vempty = vfull + kCapR / 2;                                     // H -> V
 
   const int tid = threadIdx.x;
   // warp index as a warp-uniform value and lane id from the special register (kept in registers, not
@@ -279,9 +284,9 @@ resize_fast_kernel(FKParams kp, const vp_clip_plan* __restrict__ plans, int n, c
   const int64_t my_b = it_begin + total * (blockIdx.x + 1) / gridDim.x;
 
   if (tid == 0) {
-    for (int s = 0; s < kNVW * kDepth; ++s) mbar_init(&full_all[s], 1);
-    for (int s = 0; s < kCapR; ++s) {
-      mbar_init(&vfull[s], kNVW);
+    for (int s = 0; s < kNVW * kNGrp; ++s) mbar_init(&full_all[s], 1);
+    for (int s = 0; s < kCapR / 2; ++s) {
+      mbar_init(&vfull[s], 2 * kNVW);      // each V warp arrives once per row of the pair
       mbar_init(&vempty[s], kNHW);
     }
     asm volatile("fence.mbarrier_init.release.cluster;" ::: "memory");
@@ -293,7 +298,7 @@ resize_fast_kernel(FKParams kp, const vp_clip_plan* __restrict__ plans, int n, c
     // ============================================================ V warps: vertical ring
     asm volatile("setmaxnreg.inc.sync.aligned.u32 152;\n" ::: "memory");
     uint8_t* stage = stage_all + (size_t)warp * kDepth * kWarpB;
-    uint64_t* full = full_all + warp * kDepth;
+    uint64_t* full = full_all + warp * kNGrp;     // one barrier per group of kGrp staging slots
     uint32_t rslot = 0, rphase = 0;   // staging ring position of the next row to read
     uint32_t vrow = 0;                // running count of retired rows (vbuf slot = vrow % kCapR)
     int cached_clip = -1;
@@ -301,7 +306,7 @@ resize_fast_kernel(FKParams kp, const vp_clip_plan* __restrict__ plans, int n, c
     ProdItem pit = {nullptr, 0, my_a, 0, 0};
     const uint8_t* psrc = nullptr;
     int prows = 0;
-    auto issue = [&](uint32_t slot) {
+    auto issue = [&](uint32_t slot) {             // one row into staging slot `slot` (group barrier slot/4)
       if (prows == 0) {
         if (pit.src != nullptr || pit.item == my_a) {
           pit = producer_open<VARIANT>(plans, n, warp, frames, clip_off, pitch_arr,
@@ -313,16 +318,19 @@ resize_fast_kernel(FKParams kp, const vp_clip_plan* __restrict__ plans, int n, c
         if (prows == 0) return;
       }
       if (pit.nbytes > 0) {
-        mbar_arrive_expect_tx(&full[slot], (uint32_t)pit.nbytes);
-        tma_bulk_g2s(stage + (size_t)slot * kWarpB, psrc, (uint32_t)pit.nbytes, &full[slot]);
-      } else {
-        mbar_arrive(&full[slot]);                                   // empty slice: complete the phase
+        mbar_expect_tx(&full[slot / kGrp], (uint32_t)pit.nbytes);
+        tma_bulk_g2s(stage + (size_t)slot * kWarpB, psrc, (uint32_t)pit.nbytes, &full[slot / kGrp]);
       }
       psrc += pit.pitch;
       --prows;
     };
+    auto issue_group = [&](uint32_t g) {          // refill the kGrp slots of group g, then arrive once
+#pragma unroll
+      for (int q = 0; q < kGrp; ++q) issue(g * kGrp + q);
+      mbar_arrive(&full[g]);
+    };
     if (lane == 0)
-      for (uint32_t q = 0; q < kDepth; ++q) issue(q);     // prefill
+      for (uint32_t g = 0; g < kNGrp; ++g) issue_group(g);     // prefill
     int64_t item = my_a;
     while (item < my_b) {
       const int k = find_clip_f(plans, n, item);
@@ -391,7 +399,7 @@ resize_fast_kernel(FKParams kp, const vp_clip_plan* __restrict__ plans, int n, c
         uint32_t n0 = 0, n1 = 0, n2 = 0;
         float4 nwa = make_float4(0.f, 0.f, 0.f, 0.f), nwb = nwa;
         auto load_row = [&](int yy) {
-          mbar_wait(&full[rslot], rphase);
+          if ((rslot & (kGrp - 1)) == 0) mbar_wait(&full[rslot / kGrp], rphase);   // once per group
           const uint32_t* sp = reinterpret_cast<const uint32_t*>(stage + rslot * kWarpB) + lane * 3;
           n0 = sp[0]; n1 = sp[1]; n2 = sp[2];
           const float4* wp = reinterpret_cast<const float4*>(wrow + 8 * yy);
@@ -416,7 +424,7 @@ resize_fast_kernel(FKParams kp, const vp_clip_plan* __restrict__ plans, int n, c
               if (y + 1 < in_h) load_row(y + 1);                                                \
               if ((used & 3) == 3) {                                                            \
                 __syncwarp();                                                                   \
-                if (lane == 0) { issue(used - 3); issue(used - 2); issue(used - 1); issue(used); } \
+                if (lane == 0) issue_group(used / kGrp); \
               }                                                                                 \
               float2 fv[6];                                                                     \
               fv[0] = make_float2((float)(r0 & 0xffu), (float)((r0 >> 8) & 0xffu));            \
@@ -428,16 +436,21 @@ resize_fast_kernel(FKParams kp, const vp_clip_plan* __restrict__ plans, int n, c
               const float w5[kRing] = {wa.x, wa.y, wa.z, wa.w, wb.x};                           \
               ring_row<U>(acc, w5, fv);                                                         \
             }                                                                                   \
-            const uint32_t vs = vrow % kCapR, vph = (vrow / kCapR) & 1;                         \
-            mbar_wait(&vempty[vs], vph ^ 1);                                                    \
+            const uint32_t vs = vrow % kCapR, vp2 = vs >> 1, vph = (vrow / kCapR) & 1;          \
+            if ((vrow & 1) == 0) mbar_wait(&vempty[vp2], vph ^ 1);    /* once per row pair */   \
             retire_slot<U>(acc, vdst_base + vs * kRowPx, vactive);                              \
             __syncwarp();                                                                       \
-            if (lane == 0) mbar_arrive(&vfull[vs]);                                             \
+            if (lane == 0) mbar_arrive(&vfull[vp2]);                                            \
             ++vrow;                                                                             \
           }
           static_assert(kRing == 5, "unroll below");
           VP_ROW(0) VP_ROW(1) VP_ROW(2) VP_ROW(3) VP_ROW(4)
 #undef VP_ROW
+        }
+        if (vrow & 1) {                             // odd out_h: complete the last pair's barrier phase
+          __syncwarp();
+          if (lane == 0) mbar_arrive(&vfull[(vrow % kCapR) >> 1]);
+          ++vrow;
         }
         // the row prefetched beyond the last window (if any) and all rows below it keep the ring in step
         if (y < in_h) {
@@ -445,19 +458,19 @@ resize_fast_kernel(FKParams kp, const vp_clip_plan* __restrict__ plans, int n, c
           if (++rslot == kDepth) { rslot = 0; rphase ^= 1; }
           if ((used & 3) == 3) {
             __syncwarp();
-            if (lane == 0) { issue(used - 3); issue(used - 2); issue(used - 1); issue(used); }
+            if (lane == 0) issue_group(used / kGrp);
           }
           ++y;
         }
         // source rows below the last window (none for the supported ratios) keep the ring in step
         for (; y < in_h; ++y) {
-          mbar_wait(&full[rslot], rphase);
+          if ((rslot & (kGrp - 1)) == 0) mbar_wait(&full[rslot / kGrp], rphase);
           __syncwarp();
           const uint32_t used = rslot;
           if (++rslot == kDepth) { rslot = 0; rphase ^= 1; }
           if ((used & 3) == 3) {
             __syncwarp();
-            if (lane == 0) { issue(used - 3); issue(used - 2); issue(used - 1); issue(used); }
+            if (lane == 0) issue_group(used / kGrp);
           }
         }
       }
@@ -530,10 +543,8 @@ resize_fast_kernel(FKParams kp, const vp_clip_plan* __restrict__ plans, int n, c
 
       for (int i = 0; i < out_h; i += 2) {
         const bool two = i + 1 < out_h;
-        const uint32_t s0 = vrow % kCapR, ph0 = (vrow / kCapR) & 1;
-        const uint32_t s1 = (vrow + 1) % kCapR, ph1 = ((vrow + 1) / kCapR) & 1;
-        mbar_wait(&vfull[s0], ph0);
-        if (two) mbar_wait(&vfull[s1], ph1);
+        const uint32_t s0 = vrow % kCapR, s1 = s0 + 1, ph0 = (vrow / kCapR) & 1;   // rows of pair s0/2
+        mbar_wait(&vfull[s0 >> 1], ph0);
         const int64_t rp0 = base0 + r_hb * hb_stride + (int64_t)(r_mh * m) * kp.D + r_py * p;
         if (++r_py == p) { r_py = 0; if (++r_mh == m) { r_mh = 0; ++r_hb; } }
         const int64_t rp1 = base0 + r_hb * hb_stride + (int64_t)(r_mh * m) * kp.D + r_py * p;
@@ -612,11 +623,8 @@ resize_fast_kernel(FKParams kp, const vp_clip_plan* __restrict__ plans, int n, c
           }
         }
         __syncwarp();
-        if (lane == 0) {
-          mbar_arrive(&vempty[s0]);
-          if (two) mbar_arrive(&vempty[s1]);
-        }
-        vrow += two ? 2 : 1;
+        if (lane == 0) mbar_arrive(&vempty[s0 >> 1]);
+        vrow += 2;                                  // V pads an odd last row, so pairs stay aligned
       }
     }
   }
