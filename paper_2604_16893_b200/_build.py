@@ -32,8 +32,9 @@ def build(verbose: bool = False, force: bool = False) -> str:
     objs = []
     for s in SOURCES:
         o = os.path.join(objdir, s.replace(".cu", ".o"))
+        extra = os.environ.get("VP_EXTRA_NVCC_FLAGS", "").split()   # experiments only
         cmd = [nvcc(), *ARCH, "-O3", "-lineinfo", "-std=c++17", "-Xcompiler", "-fPIC", "-Xptxas", "-v",
-               "--expt-relaxed-constexpr", *PER_FILE.get(s, []), "-c", os.path.join(CSRC, s), "-o", o]
+               "--expt-relaxed-constexpr", *PER_FILE.get(s, []), *extra, "-c", os.path.join(CSRC, s), "-o", o]
         r = subprocess.run(cmd, capture_output=True, text=True)
         if r.returncode != 0:
             raise RuntimeError(f"nvcc failed for {s}:\n{r.stderr}")
