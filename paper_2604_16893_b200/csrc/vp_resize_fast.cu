@@ -40,6 +40,8 @@ constexpr int kRowPx = kFastPx + 48;      // float4 pixels per buffered row (+ t
 struct FKParams {
   int p, m, tp, D;
   float scale[3], bias[3];
+  float lo[3], hi[3];               // output-domain clamp bounds: bias, fma(255, scale, bias)
+  __nv_bfloat162 lo2[3], hi2[3];    // the same, RNE to bf16, duplicated
 };
 
 // ---------------------------------------------------------------- PTX helpers (mbarrier / TMA bulk)
@@ -572,42 +574,52 @@ resize_fast_kernel(FKParams kp, const vp_clip_plan* __restrict__ plans, int n, c
             b10 = fmaf(wp.y, q0.z, b10);
             b11 = fmaf(wp.y, q1.z, b11);
           }
-          // clamp (C12), normalise (O6): x = v*scale_c + bias_c; store (col ja, ja+1) pairs
-          const float xr0a = fmaf(fminf(fmaxf(rg00.x, 0.f), 255.f), kp.scale[0], kp.bias[0]);
-          const float xr0b = fmaf(fminf(fmaxf(rg10.x, 0.f), 255.f), kp.scale[0], kp.bias[0]);
-          const float xg0a = fmaf(fminf(fmaxf(rg00.y, 0.f), 255.f), kp.scale[1], kp.bias[1]);
-          const float xg0b = fmaf(fminf(fmaxf(rg10.y, 0.f), 255.f), kp.scale[1], kp.bias[1]);
-          const float xb0a = fmaf(fminf(fmaxf(b00, 0.f), 255.f), kp.scale[2], kp.bias[2]);
-          const float xb0b = fmaf(fminf(fmaxf(b10, 0.f), 255.f), kp.scale[2], kp.bias[2]);
-          const float xr1a = fmaf(fminf(fmaxf(rg01.x, 0.f), 255.f), kp.scale[0], kp.bias[0]);
-          const float xr1b = fmaf(fminf(fmaxf(rg11.x, 0.f), 255.f), kp.scale[0], kp.bias[0]);
-          const float xg1a = fmaf(fminf(fmaxf(rg01.y, 0.f), 255.f), kp.scale[1], kp.bias[1]);
-          const float xg1b = fmaf(fminf(fmaxf(rg11.y, 0.f), 255.f), kp.scale[1], kp.bias[1]);
-          const float xb1a = fmaf(fminf(fmaxf(b01, 0.f), 255.f), kp.scale[2], kp.bias[2]);
-          const float xb1b = fmaf(fminf(fmaxf(b11, 0.f), 255.f), kp.scale[2], kp.bias[2]);
+          // normalise (O6) x = v*scale_c + bias_c as FFMA2 over the column pair, then clamp (C12) in the
+          // output domain: clamp(v,0,255)*s+b == clamp(v*s+b, b, 255*s+b) (s > 0), and for bf16
+          // RNE(clamp(x)) == clamp(RNE(x), RNE(lo), RNE(hi)) (RNE is monotone) -> packed bf16x2 min/max.
+          const float2 s0 = make_float2(kp.scale[0], kp.scale[0]), o0 = make_float2(kp.bias[0], kp.bias[0]);
+          const float2 s1 = make_float2(kp.scale[1], kp.scale[1]), o1 = make_float2(kp.bias[1], kp.bias[1]);
+          const float2 s2 = make_float2(kp.scale[2], kp.scale[2]), o2 = make_float2(kp.bias[2], kp.bias[2]);
+          const float2 nr0 = __ffma2_rn(make_float2(rg00.x, rg10.x), s0, o0);
+          const float2 ng0 = __ffma2_rn(make_float2(rg00.y, rg10.y), s1, o1);
+          const float2 nb0 = __ffma2_rn(make_float2(b00, b10), s2, o2);
+          const float2 nr1 = __ffma2_rn(make_float2(rg01.x, rg11.x), s0, o0);
+          const float2 ng1 = __ffma2_rn(make_float2(rg01.y, rg11.y), s1, o1);
+          const float2 nb1 = __ffma2_rn(make_float2(b01, b11), s2, o2);
+          auto clampf2 = [&](float2 v, int c) {
+            return make_float2(fminf(fmaxf(v.x, kp.lo[c]), kp.hi[c]), fminf(fmaxf(v.y, kp.lo[c]), kp.hi[c]));
+          };
+          auto packbf = [&](float2 v, int c) {
+            const __nv_bfloat162 q = __floats2bfloat162_rn(v.x, v.y);
+            return __hmin2(__hmax2(q, kp.lo2[c]), kp.hi2[c]);
+          };
+          const float2 xr0 = clampf2(nr0, 0), xg0 = clampf2(ng0, 1), xb0 = clampf2(nb0, 2);
+          const float2 xr1 = clampf2(nr1, 0), xg1 = clampf2(ng1, 1), xb1 = clampf2(nb1, 2);
+          const float xr0a = xr0.x, xr0b = xr0.y, xg0a = xg0.x, xg0b = xg0.y, xb0a = xb0.x, xb0b = xb0.y;
+          const float xr1a = xr1.x, xr1b = xr1.y, xg1a = xg1.x, xg1b = xg1.y, xb1a = xb1.x, xb1b = xb1.y;
           if (nslots == 1) {
             // common case: one temporal slot -> 3 (or 6) stores at constant channel offsets from a row pointer
             if (kF32) {
               float* q0 = reinterpret_cast<float*>(pv) + rp0 + colpart;
-              *reinterpret_cast<float2*>(q0) = make_float2(xr0a, xr0b);
-              *reinterpret_cast<float2*>(q0 + cstride) = make_float2(xg0a, xg0b);
-              *reinterpret_cast<float2*>(q0 + 2 * cstride) = make_float2(xb0a, xb0b);
+              *reinterpret_cast<float2*>(q0) = xr0;
+              *reinterpret_cast<float2*>(q0 + cstride) = xg0;
+              *reinterpret_cast<float2*>(q0 + 2 * cstride) = xb0;
               if (two) {
                 float* q1 = reinterpret_cast<float*>(pv) + rp1 + colpart;
-                *reinterpret_cast<float2*>(q1) = make_float2(xr1a, xr1b);
-                *reinterpret_cast<float2*>(q1 + cstride) = make_float2(xg1a, xg1b);
-                *reinterpret_cast<float2*>(q1 + 2 * cstride) = make_float2(xb1a, xb1b);
+                *reinterpret_cast<float2*>(q1) = xr1;
+                *reinterpret_cast<float2*>(q1 + cstride) = xg1;
+                *reinterpret_cast<float2*>(q1 + 2 * cstride) = xb1;
               }
             } else {
               __nv_bfloat16* q0 = reinterpret_cast<__nv_bfloat16*>(pv) + rp0 + colpart;
-              *reinterpret_cast<__nv_bfloat162*>(q0) = __floats2bfloat162_rn(xr0a, xr0b);
-              *reinterpret_cast<__nv_bfloat162*>(q0 + cstride) = __floats2bfloat162_rn(xg0a, xg0b);
-              *reinterpret_cast<__nv_bfloat162*>(q0 + 2 * cstride) = __floats2bfloat162_rn(xb0a, xb0b);
+              *reinterpret_cast<__nv_bfloat162*>(q0) = packbf(nr0, 0);
+              *reinterpret_cast<__nv_bfloat162*>(q0 + cstride) = packbf(ng0, 1);
+              *reinterpret_cast<__nv_bfloat162*>(q0 + 2 * cstride) = packbf(nb0, 2);
               if (two) {
                 __nv_bfloat16* q1 = reinterpret_cast<__nv_bfloat16*>(pv) + rp1 + colpart;
-                *reinterpret_cast<__nv_bfloat162*>(q1) = __floats2bfloat162_rn(xr1a, xr1b);
-                *reinterpret_cast<__nv_bfloat162*>(q1 + cstride) = __floats2bfloat162_rn(xg1a, xg1b);
-                *reinterpret_cast<__nv_bfloat162*>(q1 + 2 * cstride) = __floats2bfloat162_rn(xb1a, xb1b);
+                *reinterpret_cast<__nv_bfloat162*>(q1) = packbf(nr1, 0);
+                *reinterpret_cast<__nv_bfloat162*>(q1 + cstride) = packbf(ng1, 1);
+                *reinterpret_cast<__nv_bfloat162*>(q1 + 2 * cstride) = packbf(nb1, 2);
               }
             }
           } else {
@@ -668,6 +680,10 @@ void launch_resize_fast(const vp_params* p, const vp_clip_plan* plans, int n, co
   for (int c = 0; c < 3; ++c) {
     kp.scale[c] = (float)(1.0 / (255.0 * p->std[c]));
     kp.bias[c] = (float)(-p->mean[c] / p->std[c]);
+    kp.lo[c] = kp.bias[c];
+    kp.hi[c] = fmaf(255.0f, kp.scale[c], kp.bias[c]);
+    kp.lo2[c] = __floats2bfloat162_rn(kp.lo[c], kp.lo[c]);
+    kp.hi2[c] = __floats2bfloat162_rn(kp.hi[c], kp.hi[c]);
   }
   if (p->out_dtype == VP_OUT_F32) {
     launch_fast<KV_MILD, true>(kp, plans, n, frames, coff, pitch, pi, icap, pvv, vcap, s);
