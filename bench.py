@@ -109,11 +109,17 @@ def run_ours(args, rank, world, local_rank):
 
     torch.cuda.set_device(local_rank)
     dev = torch.device("cuda", local_rank)
-    job_clips = args.clips if args.clips else JOB_CLIPS
+    if args.config == "cfg5":
+        job_clips = args.clips if args.clips else JOB_CLIPS
+        params, all_clips = cfg5_params(), [cfg5_clip()] * job_clips
+    else:                                   # other BASELINE configs (profiling / reporting only)
+        params, all_clips = I.config(args.config)
+        job_clips = len(all_clips)
+    from paper_2604_16893_b200.dist import shard_range
     assert job_clips % world == 0, "clips must divide evenly over ranks"
-    per = job_clips // world
-    params = cfg5_params()
-    clips = [cfg5_clip()] * per
+    a, b = shard_range(job_clips, world, rank)
+    clips = all_clips[a:b]
+    per = len(clips)
     pre = vp.VisualPreprocessor(device=dev, **params)
     P = pre.params
     m = P.merge_size
@@ -136,10 +142,14 @@ def run_ours(args, rank, world, local_rank):
     for k in range(per):
         gt, gh, gw = int(ph["grid_t"][k]), int(ph["grid_h"][k]), int(ph["grid_w"][k])
         runs = [(0, 64)]
-        for _ in range(gt):
-            runs += [(0, 7), (2, gh * gw // (m * m)), (0, 1)]
+        if ph["is_image"][k]:
+            runs += [(0, 1), (1, gh * gw // (m * m)), (0, 1)]
+        else:
+            for _ in range(gt):
+                runs += [(0, 7), (2, gh * gw // (m * m)), (0, 1)]
         runs.append((0, 32))
         seqs.append(I.token_types(runs))
+    n_img = int(pl.totals["n_images"])
     tt = torch.from_numpy(np.concatenate(seqs)).to(dev)
     cu = torch.tensor(np.concatenate([[0], np.cumsum([len(s) for s in seqs])]), dtype=torch.int64, device=dev)
     L = tt.numel()
@@ -169,13 +179,15 @@ def run_ours(args, rank, world, local_rank):
             a = torch.cuda.Event(enable_timing=True)
             b = torch.cuda.Event(enable_timing=True)
             a.record(stream)
-        vp.resize_normalize_patchify(P, pl.plans_dev, per, frames, off_d, pitch_d, None,
+        vp.resize_normalize_patchify(P, pl.plans_dev, per, frames, off_d, pitch_d,
+                                     out["pixel_values"] if n_img else None,
                                      out["pixel_values_videos"], out["image_grid_thw"], out["video_grid_thw"],
                                      out["clip_status"])
         if record:
             b.record(stream)
             ev_k3.append((a, b))
-        vp.rope_index(P, vp.VP_ROPE_QWEN3_SPLIT, tt, cu, None, out["video_grid_thw"], pos, deltas, rst, ws)
+        vp.rope_index(P, vp.VP_ROPE_QWEN3_SPLIT, tt, cu, out["image_grid_thw"] if n_img else None,
+                      out["video_grid_thw"], pos, deltas, rst, ws)
 
     launches_per_step = 5 + (2 if world > 1 else 0)
     for _ in range(args.warmup):
@@ -209,7 +221,7 @@ def run_ours(args, rank, world, local_rank):
 
     # ---------------- e2e: pinned host frames -> device inside the timed region ----------------
     e2e = None
-    if not args.no_e2e:
+    if not args.no_e2e and args.config == "cfg5":
         e2e = run_e2e(args, pre, pl, frames, off, pitch, out, tt, cu, pos, deltas, rst, ws, per, dev, world,
                       tokens_rank)
 
@@ -223,9 +235,10 @@ def run_ours(args, rank, world, local_rank):
             "metric": METRIC, "value": tokens_job / (ms_step * 1e-3), "unit": UNIT, "n_gpus": world,
             "steps": args.steps, "warmup": args.warmup, "ms_per_step": ms_step, "higher_is_better": True,
             "scaling": "strong", "vs_baseline": None, "dtype": "f32", "data": "synthetic",
-            "config": {"workload": f"cfg5: GRPO rollout batch of {job_clips} clips (cfg2-shaped: 30 fps 1280x720, "
-                                   f"2 fps, <=64 frames, 262144 px/frame -> 384x672, grid (32,24,42)) sharded by "
-                                   f"clip over {world} rank(s)",
+            "config": {"workload": (f"cfg5: GRPO rollout batch of {job_clips} clips (cfg2-shaped: 30 fps 1280x720, "
+                                    f"2 fps, <=64 frames, 262144 px/frame -> 384x672, grid (32,24,42)) sharded by "
+                                    f"clip over {world} rank(s)") if args.config == "cfg5" else
+                                   f"{args.config} (BASELINE.json configs[{args.config[-1]}]), {job_clips} clips",
                        "clips_per_rank": per, "tokens_per_step": tokens_job,
                        "out_dtype": "bf16" if P.out_dtype == 0 else "f32", "model_preset": "Qwen3-VL p16 m2 tp2",
                        "l2": "inputs (%.1f GB/rank) larger than L2, no flush" % (in_bytes / 1e9),
@@ -403,6 +416,8 @@ def main():
     ap.add_argument("--warmup", type=int, default=3)
     ap.add_argument("--impl", default="ours", choices=["ours", "reference"])
     ap.add_argument("--clips", type=int, default=0, help="override job clip count (profiling only)")
+    ap.add_argument("--config", default="cfg5", choices=["cfg5", "cfg1", "cfg2", "cfg3", "cfg4"],
+                    help="workload (default cfg5, the metric's configuration)")
     ap.add_argument("--no-e2e", action="store_true")
     ap.add_argument("--e2e-steps", type=int, default=2)
     ap.add_argument("--e2e-chunk", type=int, default=8)
