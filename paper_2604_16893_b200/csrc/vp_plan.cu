@@ -83,8 +83,14 @@ __device__ ClipResult plan_one(const vp_params& P, const vp_clip_desc& c) {
 
 // Center-of-bin index: min(total-1, floor((2i+1)*total / (2n))) in exact integers.
 __device__ __forceinline__ int64_t frame_index(int64_t i, int64_t total, int64_t n) {
-  unsigned __int128 num = (unsigned __int128)(2 * i + 1) * (unsigned __int128)total;
-  int64_t q = (int64_t)(num / (unsigned __int128)(2 * n));
+  const uint64_t a = (uint64_t)(2 * i + 1), t = (uint64_t)total;
+  int64_t q;
+  if (a <= (~0ull) / t) {                              // product fits 64 bits: plain u64 division
+    q = (int64_t)((a * t) / (uint64_t)(2 * n));
+  } else {
+    unsigned __int128 num = (unsigned __int128)a * (unsigned __int128)t;
+    q = (int64_t)(num / (unsigned __int128)(2 * n));
+  }
   return q < total - 1 ? q : total - 1;
 }
 
@@ -94,14 +100,9 @@ plan_kernel(vp_params P, const vp_clip_desc* __restrict__ clips, int n, vp_clip_
             int64_t* __restrict__ totals) {
   __shared__ int64_t warp_tot[32][kNScan];
   __shared__ int64_t carry[kNScan];
-  __shared__ int32_t s_n[kPlanThreads], s_isimg[kPlanThreads], s_ok[kPlanThreads];
-  __shared__ int64_t s_ioff[kPlanThreads], s_total[kPlanThreads], s_goff[kPlanThreads];
-  __shared__ double s_fps[kPlanThreads];
-  __shared__ int64_t s_flags;
   const int tid = threadIdx.x, lane = tid & 31, warp = tid >> 5;
   const int64_t m2 = (int64_t)P.merge_size * P.merge_size;
   if (tid < kNScan) carry[tid] = 0;
-  if (tid == 0) s_flags = 0;
   __syncthreads();
 
   for (int base = 0; base < n; base += kPlanThreads) {
@@ -183,48 +184,10 @@ plan_kernel(vp_params P, const vp_clip_desc* __restrict__ clips, int n, vp_clip_
       pl.tile_offset = ex[S_TILES];   // monotone over all clips (invalid clips: count 0)
       plans[k] = pl;
     }
-    s_n[tid] = ok ? r.n : 0;
-    s_isimg[tid] = r.is_image;
-    s_ok[tid] = ok;
-    s_ioff[tid] = ex[S_IDX];
-    s_total[tid] = r.total;
-    s_fps[tid] = r.src_fps;
-    s_goff[tid] = ex[S_GROUPS];
     __syncthreads();
     if (tid == kPlanThreads - 1) {
 #pragma unroll
       for (int j = 0; j < kNScan; ++j) carry[j] = ex[j] + v[j];
-    }
-    // ---- frame indices (O1) and group timestamps (O10): one warp per clip ----
-    const int nchunk = min(kPlanThreads, n - base);
-    const int64_t tp = P.temporal_patch_size;
-    for (int c = warp; c < nchunk; c += kPlanThreads / 32) {
-      if (!s_ok[c]) continue;
-      const int64_t nn = s_n[c], off = s_ioff[c];
-      if (s_isimg[c]) {
-        if (lane == 0) {
-          if (off < index_cap) frame_indices[off] = 0;
-          else atomicOr((unsigned long long*)&s_flags, 1ull);
-        }
-        continue;
-      }
-      const int64_t total = s_total[c];
-      for (int64_t i = lane; i < nn; i += 32) {
-        if (off + i < index_cap) frame_indices[off + i] = frame_index(i, total, nn);
-        else atomicOr((unsigned long long*)&s_flags, 1ull);
-      }
-      if (ts != nullptr) {
-        const double fps = s_fps[c];
-        const int64_t groups = ceil_div(nn, tp);
-        for (int64_t g = lane; g < groups; g += 32) {
-          int64_t i0 = g * tp, i1 = min(g * tp + tp - 1, nn - 1);   // pad with last index (C22)
-          double a = __ddiv_rn((double)frame_index(i0, total, nn), fps);
-          double b = __ddiv_rn((double)frame_index(i1, total, nn), fps);
-          const int64_t o = s_goff[c] + g;
-          if (o < ts_cap) ts[o] = __dmul_rn(__dadd_rn(a, b), 0.5);
-          else atomicOr((unsigned long long*)&s_flags, 2ull);
-        }
-      }
     }
     __syncthreads();
   }
@@ -238,10 +201,53 @@ plan_kernel(vp_params P, const vp_clip_desc* __restrict__ clips, int n, vp_clip_
     totals[VP_TOT_N_VIDEOS] = carry[S_NVID];
     totals[VP_TOT_VID_GROUPS] = carry[S_GROUPS];
     totals[VP_TOT_TILES] = carry[S_TILES];
-    totals[VP_TOT_FLAGS] = s_flags;
+    totals[VP_TOT_FLAGS] = 0;                     // plan_fill_kernel ORs overflow bits in
     totals[VP_TOT_N_INVALID] = carry[S_INVALID];
     totals[11] = 0;
   }
+}
+
+
+// ---- frame indices (O1) and group timestamps (O10): one warp per clip, many CTAs (the per-frame
+//      integer divisions dominate K1 for long clips, so they are spread over the whole GPU) ----
+constexpr int kFillThreads = 256;
+__global__ void __launch_bounds__(kFillThreads)
+plan_fill_kernel(int64_t tp, const vp_clip_desc* __restrict__ clips, int n, const vp_clip_plan* __restrict__ plans,
+                 int64_t* __restrict__ frame_indices, int64_t index_cap, double* __restrict__ ts, int64_t ts_cap,
+                 int64_t* __restrict__ totals) {
+  const int lane = threadIdx.x & 31;
+  const int c = blockIdx.x * (kFillThreads / 32) + (threadIdx.x >> 5);
+  if (c >= n) return;
+  const vp_clip_plan& pl = plans[c];
+  if (pl.status != VP_OK) return;
+  unsigned long long flags = 0;
+  const int64_t nn = pl.n_frames, off = pl.index_offset;
+  if (pl.is_image) {
+    if (lane == 0) {
+      if (off < index_cap) frame_indices[off] = 0;
+      else flags |= 1ull;
+    }
+  } else {
+    const int64_t total = clips[c].total_source_frames;
+    for (int64_t i = lane; i < nn; i += 32) {
+      if (off + i < index_cap) frame_indices[off + i] = frame_index(i, total, nn);
+      else flags |= 1ull;
+    }
+    if (ts != nullptr) {
+      const double fps = clips[c].source_fps;
+      const int64_t groups = ceil_div(nn, tp);
+      for (int64_t g = lane; g < groups; g += 32) {
+        int64_t i0 = g * tp, i1 = min(g * tp + tp - 1, nn - 1);   // pad with last index (C22)
+        double a = __ddiv_rn((double)frame_index(i0, total, nn), fps);
+        double b = __ddiv_rn((double)frame_index(i1, total, nn), fps);
+        const int64_t o = pl.group_offset + g;
+        if (o < ts_cap) ts[o] = __dmul_rn(__dadd_rn(a, b), 0.5);
+        else flags |= 2ull;
+      }
+    }
+  }
+  flags = __reduce_or_sync(0xffffffffu, (unsigned)flags);
+  if (lane == 0 && flags) atomicOr((unsigned long long*)&totals[VP_TOT_FLAGS], flags);
 }
 
 }  // namespace
@@ -264,5 +270,10 @@ extern "C" vp_status vp_plan_frames(const vp_params* p, const vp_clip_desc* clip
   }
   vp::plan_kernel<<<1, vp::kPlanThreads, 0, vp::as_stream(stream)>>>(*p, clips, n, plans, frame_indices,
                                                                       index_cap, group_timestamps, ts_cap, totals);
+  if (n > 0) {
+    const int per = vp::kFillThreads / 32;
+    vp::plan_fill_kernel<<<(n + per - 1) / per, vp::kFillThreads, 0, vp::as_stream(stream)>>>(
+        p->temporal_patch_size, clips, n, plans, frame_indices, index_cap, group_timestamps, ts_cap, totals);
+  }
   return vp::launch_status("vp_plan_frames");
 }

@@ -104,17 +104,52 @@ resize_generic_kernel(KParams kp, const vp_clip_plan* __restrict__ plans, int n,
   // Clips this kernel owns: KV_GENERIC, or fast-variant clips whose buffers are not 16-B aligned
   // (the fast kernel's TMA row copies need 16-B aligned rows).  Token tiles of every owned clip are
   // dealt round-robin over the CTAs, continuing the rotation across clips.
-  int cached_clip = -1;
+  // The plan list is scanned 256 clips at a time by the whole CTA (one clip per thread, block scan of
+  // the owned tile counts), so a batch with no generic clip costs ~n/256 parallel steps, not n serial
+  // plan loads per CTA.
+  __shared__ int s_list[kThreads];
+  __shared__ int64_t s_start[kThreads];
+  __shared__ int64_t s_wsum[kThreads / 32];
+  __shared__ int s_wcnt[kThreads / 32];
   int64_t rot = 0;
-  for (int k = 0; k < n; ++k) {
+  for (int c0 = 0; c0 < n; c0 += kThreads) {
+   const int kk = c0 + tid;
+   int64_t my_tiles = 0;
+   if (kk < n) {
+     const vp_clip_plan& q = plans[kk];
+     const bool fast_ok = fast_aligned && q.kernel_variant != KV_GENERIC && ((clip_off[kk] | pitch_arr[kk]) & 15) == 0;
+     if (q.status == VP_OK && !fast_ok) my_tiles = clip_tiles(q.grid_t, q.grid_h, q.grid_w, kp.m);
+   }
+   // block exclusive scan of (my_tiles, owned)
+   const int lane = tid & 31, wid = tid >> 5;
+   int64_t incl = my_tiles;
+   int cnt = my_tiles > 0;
+#pragma unroll
+   for (int o = 1; o < 32; o <<= 1) {
+     const int64_t a = __shfl_up_sync(0xffffffffu, incl, o);
+     const int b = __shfl_up_sync(0xffffffffu, cnt, o);
+     if (lane >= o) { incl += a; cnt += b; }
+   }
+   __syncthreads();                                  // previous chunk's s_list/s_start readers are done
+   if (lane == 31) { s_wsum[wid] = incl; s_wcnt[wid] = cnt; }
+   __syncthreads();
+   int64_t wbase = 0, total = 0;
+   int cbase = 0, ctotal = 0;
+   for (int w = 0; w < kThreads / 32; ++w) {
+     if (w < wid) { wbase += s_wsum[w]; cbase += s_wcnt[w]; }
+     total += s_wsum[w]; ctotal += s_wcnt[w];
+   }
+   if (my_tiles > 0) {
+     const int slot = cbase + cnt - 1;
+     s_list[slot] = kk;
+     s_start[slot] = rot + wbase + incl - my_tiles;
+   }
+   __syncthreads();
+   for (int li = 0; li < ctotal; ++li) {
+   const int k = s_list[li];
    const vp_clip_plan plk = plans[k];
-   if (plk.status != VP_OK) continue;
-   const bool fast_ok = fast_aligned && plk.kernel_variant != KV_GENERIC &&
-                        ((clip_off[k] | pitch_arr[k]) & 15) == 0;
-   if (fast_ok) continue;
    const int64_t ntile = clip_tiles(plk.grid_t, plk.grid_h, plk.grid_w, kp.m);
-   const int64_t first = ((int64_t)blockIdx.x - rot % gridDim.x + gridDim.x) % gridDim.x;
-   rot += ntile;
+   const int64_t first = ((int64_t)blockIdx.x - s_start[li] % gridDim.x + gridDim.x) % gridDim.x;
    for (int64_t local = first; local < ntile; local += gridDim.x) {
     const vp_clip_plan& pl = plk;
     const int gh = pl.grid_h, gw = pl.grid_w;
@@ -144,7 +179,6 @@ resize_generic_kernel(KParams kp, const vp_clip_plan* __restrict__ plans, int n,
     }
     __syncthreads();
     if (s_bad) continue;
-    (void)cached_clip;
     const int xa = s_hx0[0];
     const int xb = s_hx0[B - 1] + s_hlen[B - 1];
     const int fpb = 3 * (xb - xa);                 // footprint bytes per source row
@@ -198,6 +232,8 @@ resize_generic_kernel(KParams kp, const vp_clip_plan* __restrict__ plans, int n,
       ti = ti_end;
     }
    }
+   }
+   rot += total;
   }
 #undef s_wv
 #undef s_wh
