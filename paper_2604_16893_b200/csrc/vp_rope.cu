@@ -8,7 +8,7 @@
 // The grid of a visual run is the o-th grid of its modality in batch order, o = run ordinal.
 // Kernel A: per-sequence counts of visual runs (for batch-order ordinals) + video grid expansion
 // prefix (QWEN3_SPLIT: video v contributes grid_t grids (1,h,w)).  Kernel B: one CTA per sequence,
-// 512-token chunks, two block scans per chunk (warp shuffles), carries between chunks.
+// 4096-token chunks (8 consecutive tokens per thread), two block scans per chunk, carries between chunks.
 #include "vp_internal.cuh"
 
 namespace vp {
@@ -16,6 +16,7 @@ namespace {
 
 constexpr int kRopeThreads = 512;
 constexpr int kWarps = kRopeThreads / 32;
+constexpr int kPer = 8;           // tokens per thread in the fill kernel
 
 // Inclusive block scan of NV int64 lanes (sum), returns inclusive values; totals in tot[].
 template <int NV>
@@ -129,7 +130,7 @@ struct GridInfo {
 __device__ __forceinline__ GridInfo grid_info(int typ, int64_t o, int variant, int m, const int64_t* __restrict__ igrid,
                                               int n_images, const int64_t* __restrict__ vgrid, int n_videos,
                                               const int64_t* __restrict__ vcum, const double* __restrict__ spg,
-                                              int tps) {
+                                              int tps, int vlo, int vhi) {
   GridInfo r{};
   r.valid = false;
   r.iv = 1;
@@ -139,8 +140,8 @@ __device__ __forceinline__ GridInfo grid_info(int typ, int64_t o, int variant, i
   } else {
     if (o >= vcum[n_videos]) return r;
     int64_t v = o;
-    if (variant == VP_ROPE_QWEN3_SPLIT) {       // last v with vcum[v] <= o
-      int lo = 0, hi = n_videos - 1;
+    if (variant == VP_ROPE_QWEN3_SPLIT) {       // last v with vcum[v] <= o, searched in [vlo, vhi]
+      int lo = vlo, hi = vhi;
       while (lo < hi) {
         int mid = (lo + hi + 1) >> 1;
         if (vcum[mid] <= o) lo = mid; else hi = mid - 1;
@@ -159,7 +160,7 @@ __device__ __forceinline__ GridInfo grid_info(int typ, int64_t o, int variant, i
   return r;
 }
 
-__global__ void __launch_bounds__(kRopeThreads)
+__global__ void __launch_bounds__(kRopeThreads, 2)
 rope_fill_kernel(const int8_t* __restrict__ tt, const int64_t* __restrict__ cu, int B, int variant, int m,
                  const int64_t* __restrict__ igrid, int n_images, const int64_t* __restrict__ vgrid, int n_videos,
                  const double* __restrict__ spg, int tps, const int64_t* __restrict__ counts,
@@ -168,7 +169,7 @@ rope_fill_kernel(const int8_t* __restrict__ tt, const int64_t* __restrict__ cu, 
   __shared__ int64_t sh3[kWarps][3];
   __shared__ int64_t sh2[kWarps][2];
   __shared__ int64_t shm[kWarps];
-  __shared__ int s_bad;
+  __shared__ int s_bad, s_vlo, s_vhi;
   const int b = blockIdx.x, tid = threadIdx.x;
   // batch-order base ordinals of this sequence's visual runs
   int64_t bi = 0, bv = 0, ai = 0, av = 0;
@@ -187,87 +188,158 @@ rope_fill_kernel(const int8_t* __restrict__ tt, const int64_t* __restrict__ cu, 
     const int64_t n_vg = vcum[n_videos];
     status[B] = (ai == n_images && av == n_vg) ? VP_OK : VP_EMISMATCH;
   }
-  if (tid == 0) s_bad = 0;
+  if (tid == 0) {
+    s_bad = 0;
+    // videos this sequence's runs can map to (QWEN3_SPLIT): those holding ordinals [bv, bv + its runs)
+    int lo = 0, hi = n_videos > 0 ? n_videos - 1 : 0;
+    if (variant == VP_ROPE_QWEN3_SPLIT && n_videos > 0) {
+      auto find = [&](int64_t o) {
+        int a = 0, z = n_videos - 1;
+        while (a < z) {
+          const int mid = (a + z + 1) >> 1;
+          if (vcum[mid] <= o) a = mid; else z = mid - 1;
+        }
+        return a;
+      };
+      const int64_t nv = counts[2 * b + 1];
+      lo = find(bv);
+      hi = nv > 0 ? find(bv + nv - 1) : lo;
+    }
+    s_vlo = lo;
+    s_vhi = hi;
+  }
   __syncthreads();
 
   const int64_t s = cu[b], e = cu[b + 1], L = e - s;
+  const int lane = tid & 31, warp = tid >> 5;
   int64_t c_text = 0, c_A = 0, c_ri = 0, c_rv = 0, c_start = 0;
-  for (int64_t base = 0; base < L; base += kRopeThreads) {
-    const int64_t k = base + tid;
-    const bool in = k < L;
-    const int64_t g = s + k;
-    const int typ = in ? tt[g] : 0;
-    const bool start = in && (k == 0 || tt[g - 1] != typ);
-    // scan 1: visual run starts per modality + run start position (max-scan)
-    int64_t x1[2] = {start && typ == 1 ? 1 : 0, start && typ == 2 ? 1 : 0}, t1[2];
-    block_scan_sum<2>(x1, t1, sh2);
-    // run start: max over j <= k of (start_j ? j : -1), combined with the carry from earlier chunks
-    int64_t st_pos = start ? k : -1;
-    {
-      // inclusive max-scan via warp shuffles + smem
-      const int lane = tid & 31, warp = tid >> 5;
+  // Each thread owns kPer consecutive tokens of the chunk: three local passes (run starts; text count +
+  // advances of the runs it starts; emit) around two block scans.  The grid of a run is looked up once
+  // per run start (and once for a run continuing from the previous thread); the (t, h, w) offsets of a
+  // visual token advance incrementally, so no per-token division or search remains.
+  for (int64_t base = 0; base < L; base += (int64_t)kRopeThreads * kPer) {
+    const int64_t k0 = base + (int64_t)tid * kPer;
+    int ty[kPer];
+    const int first_prev = (k0 > 0 && k0 < L) ? (int)tt[s + k0 - 1] : -1;   // -1: sequence start / idle
+    int prevt = first_prev;
+    int64_t ci = 0, cv = 0, lst = -1;
 #pragma unroll
-      for (int o = 1; o < 32; o <<= 1) {
-        int64_t y = __shfl_up_sync(0xffffffffu, st_pos, o);
-        if (lane >= o) st_pos = max(st_pos, y);
+    for (int u = 0; u < kPer; ++u) {
+      const int64_t k = k0 + u;
+      ty[u] = k < L ? (int)tt[s + k] : -1;
+      if (ty[u] >= 0 && ty[u] != prevt) {                   // run start (k == 0 always starts a run)
+        if (ty[u] == 1) ++ci;
+        else if (ty[u] == 2) ++cv;
+        lst = k;
       }
-      if (lane == 31) shm[warp] = st_pos;
-      __syncthreads();
-      for (int w = 0; w < warp; ++w) st_pos = max(st_pos, shm[w]);
-      __syncthreads();
+      prevt = ty[u];
     }
-    const int64_t run_start = st_pos >= 0 ? st_pos : c_start;
-    GridInfo gi{};
-    gi.valid = false;
-    gi.A = 0;
-    int64_t o = -1;
-    if (in && typ != 0) {
-      const int64_t ord = (typ == 1 ? c_ri + x1[0] : c_rv + x1[1]) - 1;   // run ordinal within sequence
-      o = (typ == 1 ? bi : bv) + ord;
-      gi = grid_info(typ, o, variant, m, igrid, n_images, vgrid, n_videos, vcum, spg, tps);
+    const int nextt = (k0 + kPer < L) ? (int)tt[s + k0 + kPer] : -1;
+    int64_t x1[2] = {ci, cv}, t1[2];
+    block_scan_sum<2>(x1, t1, sh2);
+    const int64_t ri0 = c_ri + x1[0] - ci, rv0 = c_rv + x1[1] - cv;   // runs started before my first token
+    // exclusive prefix max of the last run start (-> start of the run my first token continues)
+    int64_t pm = lst;
+#pragma unroll
+    for (int o = 1; o < 32; o <<= 1) {
+      const int64_t y = __shfl_up_sync(0xffffffffu, pm, o);
+      if (lane >= o) pm = max(pm, y);
     }
-    // scan 2: text tokens and run advances (exclusive)
-    const int64_t my_text = (in && typ == 0) ? 1 : 0;
-    const int64_t my_A = (start && typ != 0 && gi.valid) ? gi.A : 0;
+    if (lane == 31) shm[warp] = pm;
+    __syncthreads();
+    int64_t before = __shfl_up_sync(0xffffffffu, pm, 1);
+    if (lane == 0) before = -1;
+    int64_t chunk_last = -1;
+    for (int w = 0; w < kWarps; ++w) {
+      if (w < warp) before = max(before, shm[w]);
+      chunk_last = max(chunk_last, shm[w]);
+    }
+    __syncthreads();
+    const int64_t rs0 = before >= 0 ? before : c_start;
+
+    // pass 2: my text tokens and the advances A of the runs I start
+    int64_t my_text = 0, my_A = 0;
+    {
+      int pt = first_prev;
+      int64_t ri = ri0, rv = rv0;
+#pragma unroll
+      for (int u = 0; u < kPer; ++u) {
+        const int typ = ty[u];
+        if (typ == 0) ++my_text;
+        else if (typ > 0 && typ != pt) {
+          const int64_t o = typ == 1 ? bi + ri++ : bv + rv++;
+          const GridInfo gi = grid_info(typ, o, variant, m, igrid, n_images, vgrid, n_videos, vcum, spg, tps, s_vlo, s_vhi);
+          if (gi.valid) my_A += gi.A;
+        }
+        pt = typ;
+      }
+    }
     int64_t x2[2] = {my_text, my_A}, t2[2];
     block_scan_sum<2>(x2, t2, sh2);
-    const int64_t ex_text = x2[0] - my_text, ex_A = x2[1] - my_A;
-    if (in) {
-      int64_t p = c_text + ex_text + c_A + ex_A;
-      int64_t i0, i1, i2;
-      if (typ == 0) {
-        i0 = i1 = i2 = p;
-      } else {
-        if (k > run_start && gi.valid) p -= gi.A;
-        const int64_t j = k - run_start;
-        if (gi.valid && gi.tokens > 0) {
-          const int64_t hw = gi.hh * gi.ww;
-          i0 = p + (j / hw) * gi.iv;
-          i1 = p + (j / gi.ww) % gi.hh;
-          i2 = p + j % gi.ww;
+
+    // pass 3: emit
+    {
+      int64_t tx = c_text + x2[0] - my_text, ax = c_A + x2[1] - my_A;
+      int pt = first_prev;
+      int64_t ri = ri0, rv = rv0, run_start = rs0, run_base = 0;
+      GridInfo gi{};
+      gi.valid = false;
+      int64_t jt = 0, jh = 0, jw = 0;
+      bool have = false;
+#pragma unroll
+      for (int u = 0; u < kPer; ++u) {
+        const int typ = ty[u];
+        const int64_t k = k0 + u, g = s + k;
+        if (typ < 0) break;
+        int64_t i0, i1, i2;
+        if (typ == 0) {
+          i0 = i1 = i2 = tx + ax;
+          ++tx;
+          have = false;
         } else {
-          i0 = i1 = i2 = p;
+          if (typ != pt) {                                   // run start
+            const int64_t o = typ == 1 ? bi + ri++ : bv + rv++;
+            gi = grid_info(typ, o, variant, m, igrid, n_images, vgrid, n_videos, vcum, spg, tps, s_vlo, s_vhi);
+            run_start = k;
+            run_base = tx + ax;
+            if (gi.valid) ax += gi.A;
+            jt = jh = jw = 0;
+            have = true;
+          } else if (!have) {                                // run continued from the previous thread
+            const int64_t o = typ == 1 ? bi + ri - 1 : bv + rv - 1;
+            gi = grid_info(typ, o, variant, m, igrid, n_images, vgrid, n_videos, vcum, spg, tps, s_vlo, s_vhi);
+            run_base = tx + ax - (gi.valid ? gi.A : 0);
+            const int64_t j = k - run_start;
+            if (gi.valid && gi.tokens > 0) {
+              const int64_t hw = gi.hh * gi.ww;
+              jt = j / hw;
+              jh = (j / gi.ww) % gi.hh;
+              jw = j % gi.ww;
+            }
+            have = true;
+          }
+          if (gi.valid && gi.tokens > 0) {
+            i0 = run_base + jt * gi.iv;
+            i1 = run_base + jh;
+            i2 = run_base + jw;
+            if (++jw == gi.ww) { jw = 0; if (++jh == gi.hh) { jh = 0; ++jt; } }
+          } else {
+            i0 = i1 = i2 = run_base;
+          }
+          const int nt = u + 1 < kPer ? ty[u + 1] : nextt;
+          if (nt != typ && (!gi.valid || (k - run_start + 1) != gi.tokens)) s_bad = 1;   // C24 strict check
         }
-        const bool end = (k == L - 1) || tt[g + 1] != typ;
-        if (end && (!gi.valid || (k - run_start + 1) != gi.tokens)) s_bad = 1;   // C24 strict check
+        pos[g] = i0;
+        pos[total_L + g] = i1;
+        pos[2 * total_L + g] = i2;
+        pt = typ;
       }
-      pos[g] = i0;
-      pos[total_L + g] = i1;
-      pos[2 * total_L + g] = i2;
     }
-    // carries
     c_text += t2[0];
     c_A += t2[1];
     c_ri += t1[0];
     c_rv += t1[1];
-    {
-      // run start of the chunk's last token
-      __shared__ int64_t last_start;
-      if (tid == kRopeThreads - 1) last_start = run_start;
-      __syncthreads();
-      c_start = last_start;
-      __syncthreads();
-    }
+    if (chunk_last >= 0) c_start = chunk_last;
   }
   (void)block_max;
   if (tid == 0) {
