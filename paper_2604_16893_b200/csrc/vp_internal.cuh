@@ -10,9 +10,9 @@ namespace vp {
 
 void set_error(const char* fmt, ...);
 struct vp_clip_plan_fwd;
-void launch_resize_fast(const vp_params* p, const vp_clip_plan* plans, int n, const uint8_t* frames,
-                        const int64_t* coff, const int64_t* pitch, void* pi, int64_t icap, void* pvv, int64_t vcap,
-                        cudaStream_t s);
+cudaError_t launch_resize_fast(const vp_params* p, const vp_clip_plan* plans, int n, const uint8_t* frames,
+                               const int64_t* coff, const int64_t* pitch, void* pi, int64_t icap, void* pvv,
+                               int64_t vcap, cudaStream_t s);
 vp_status check_params(const vp_params* p);
 vp_status launch_status(const char* what);
 
@@ -50,7 +50,7 @@ constexpr int kTotLen = VP_TOT_LEN;
 // KV_GENERIC covers everything else (vp_resize.cu, token tiles).  A clip's items (tile_count)
 // are n_frames x n_strips for the fast variants, 0 for generic.  Integer / f64 exact.
 // ------------------------------------------------------------------------------------------
-enum { KV_MILD = 0, KV_MEDIUM = 1, KV_STRONG = 2, KV_GENERIC = 3 };
+enum { KV_MILD = 0, KV_MEDIUM = 1, KV_STRONG = 2, KV_GENERIC = 3, KV_COPY = 4 };
 constexpr int kRing = 5;          // vertical ring slots: max live output rows per source row for in/out > 0.8
 constexpr int kInHMax = 1088;     // source rows supported by the fast kernel's per-row weight table
 constexpr int kWListMax = 6144;   // vertical weights (sum of window lengths) held in smem
@@ -91,7 +91,14 @@ __host__ __device__ __forceinline__ int fast_strip_width(int in_w, int out_w) {
   return ws;
 }
 
-__host__ __device__ __forceinline__ int select_variant(int in_h, int in_w, int out_h, int out_w) {
+// KV_COPY: both axes identity (in == out) -- the AA weights are exactly {1} (zero taps trimmed), so the
+// resize is a copy and the kernel is a pure u8 -> normalised patch-layout transpose.  Item = (frame,
+// merge-row band, kCopyMW merge columns).  Needs an even patch size (bf16x2 / float2 element pairs).
+constexpr int kCopyMW = 8;
+__host__ __device__ __forceinline__ int copy_wchunks(int grid_w, int m) { return (grid_w / m + kCopyMW - 1) / kCopyMW; }
+
+__host__ __device__ __forceinline__ int select_variant(int in_h, int in_w, int out_h, int out_w, int p) {
+  if (in_h == out_h && in_w == out_w && (p & 1) == 0) return KV_COPY;
   const double sv = (double)in_h / (double)out_h;
   // live output rows per source row <= floor(4/s)+1 for upscale (<= 5 iff s > 0.8) and <= 5 for downscale
   // (trimmed windows; brute-forced in tests/test_oracle_pixels.py::test_live_rows_bound)

@@ -119,9 +119,11 @@ plan_kernel(vp_params P, const vp_clip_desc* __restrict__ clips, int n, vp_clip_
       v[r.is_image ? S_IMGTOK : S_VIDTOK] = patches / m2;
       v[r.is_image ? S_NIMG : S_NVID] = 1;
       v[S_GROUPS] = r.is_image ? 0 : r.gt;
-      const int kv = select_variant(clips[k].height, clips[k].width, r.out_h, r.out_w);
+      const int kv = select_variant(clips[k].height, clips[k].width, r.out_h, r.out_w, P.patch_size);
       r.variant = kv;
-      if (kv != KV_GENERIC) {
+      if (kv == KV_COPY) {
+        v[S_TILES] = (int64_t)r.n * (r.gh / P.merge_size) * copy_wchunks(r.gw, P.merge_size);
+      } else if (kv != KV_GENERIC) {
         const int ws = fast_strip_width(clips[k].width, r.out_w);
         v[S_TILES] = (int64_t)r.n * ((r.out_w + ws - 1) / ws);     // items: frames x strips
       }

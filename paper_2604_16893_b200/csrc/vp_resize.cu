@@ -1,11 +1,13 @@
 // vp_resize.cu -- K2+K3: antialiased-bicubic resize -> clamp -> rescale/normalise -> temporal pad
 // -> patchify, fused; every output element is written exactly once (O4-O9).
 //
-// Work decomposition: persistent CTAs walk a flattened tile list.  A tile is
-// (clip, temporal group g, merge-row band hb, merge-column strip wb): m*p x m*p output pixels of
-// every frame slot of the group = m^2 consecutive pixel_values rows (one LLM token).  The tile list
-// is the plans' tile_offset prefix (K1), so images and videos of any size mix in one launch.
+// This TU holds the dispatch (grids/status kernel, the fast variants of vp_resize_fast.cu, and the
+// generic kernel) and the GENERIC kernel itself, which covers every ratio and alignment the fast
+// variants do not (KV_GENERIC clips, and any clip whose frame buffer is not 16-B aligned).
 //
+// Generic work decomposition: persistent CTAs walk the token tiles of the clips they own, dealt
+// round-robin.  A tile is (clip, temporal group g, merge-row band hb, merge-column strip wb): m*p x m*p
+// output pixels of every frame slot of the group = m^2 consecutive pixel_values rows (one LLM token).
 // Per tile, the AA weights of its m*p rows and m*p columns are computed in f64 and stored as fp32
 // in shared memory (K2 as a prologue).  The separable filter then runs in two passes per source
 // frame: vertical (u8 source rows -> fp32 rows of the column footprint, in shared memory) and
@@ -61,15 +63,6 @@ __device__ int aa_window(int in, int out, int i, int* x0_out, float* w_out) {
   for (int k = 0; k < len; ++k) w_out[k] = (float)(w[k] * r);
   *x0_out = x0;
   return len;
-}
-
-__device__ __forceinline__ int find_clip(const vp_clip_plan* __restrict__ plans, int n, int64_t tile) {
-  int lo = 0, hi = n - 1;          // last k with tile_offset <= tile
-  while (lo < hi) {
-    int mid = (lo + hi + 1) >> 1;
-    if (plans[mid].tile_offset <= tile) lo = mid; else hi = mid - 1;
-  }
-  return lo;
 }
 
 template <bool kF32>
@@ -319,9 +312,14 @@ extern "C" vp_status vp_resize_normalize_patchify(const vp_params* p, const vp_c
                                                    pixel_values_images != nullptr, pixel_values_videos != nullptr,
                                                    image_grid_thw, video_grid_thw, clip_status);
   const int fast_aligned = (reinterpret_cast<uintptr_t>(frames) & 15) == 0;
-  if (fast_aligned)
-    vp::launch_resize_fast(p, plans, n, frames, clip_byte_offset, row_pitch, pixel_values_images, img_rows_cap,
-                           pixel_values_videos, vid_rows_cap, s);
+  if (fast_aligned) {
+    const cudaError_t e = vp::launch_resize_fast(p, plans, n, frames, clip_byte_offset, row_pitch, pixel_values_images,
+                                                 img_rows_cap, pixel_values_videos, vid_rows_cap, s);
+    if (e != cudaSuccess) {
+      vp::set_error("vp_resize_normalize_patchify: %s", cudaGetErrorString(e));
+      return VP_ECUDA;
+    }
+  }
   const int grid = vp::g_num_sms * 3;
   const size_t smem = vp::generic_smem_bytes(kp.m * kp.p);
   static bool attr_set = false;

@@ -51,11 +51,6 @@ __device__ __forceinline__ uint32_t smem_u32(const void* p) {
 __device__ __forceinline__ void mbar_init(uint64_t* bar, uint32_t count) {
   asm volatile("mbarrier.init.shared::cta.b64 [%0], %1;" ::"r"(smem_u32(bar)), "r"(count));
 }
-__device__ __forceinline__ void mbar_arrive_expect_tx(uint64_t* bar, uint32_t bytes) {
-  asm volatile("mbarrier.arrive.expect_tx.release.cta.shared::cta.b64 _, [%0], %1;" ::"r"(smem_u32(bar)),
-               "r"(bytes)
-               : "memory");
-}
 __device__ __forceinline__ void mbar_expect_tx(uint64_t* bar, uint32_t bytes) {
   asm volatile("mbarrier.expect_tx.relaxed.cta.shared::cta.b64 [%0], %1;" ::"r"(smem_u32(bar)), "r"(bytes) : "memory");
 }
@@ -114,17 +109,21 @@ __device__ __forceinline__ Win window_of(int in, int out, int i) {
   return w;
 }
 
-__device__ __forceinline__ int find_clip_f(const vp_clip_plan* __restrict__ plans, int n, int64_t item) {
-  int lo = 0, hi = n - 1;
+// Per-variant work index (built per call by variant_index_kernel): the variant's clips in batch order
+// (list), the exclusive prefix of their item counts (off, count+1 entries) and meta = {count, items}.
+// Every CTA of a variant's launch takes a contiguous slice of that variant's items only.
+struct VIdx {
+  const int* list;
+  const int64_t* off;
+  const int64_t* meta;
+};
+__device__ __forceinline__ int vfind(const VIdx& vx, int cnt, int64_t item) {   // last j with off[j] <= item
+  int lo = 0, hi = cnt - 1;
   while (lo < hi) {
-    int mid = (lo + hi + 1) >> 1;
-    if (plans[mid].tile_offset <= item) lo = mid; else hi = mid - 1;
+    const int mid = (lo + hi + 1) >> 1;
+    if (vx.off[mid] <= item) lo = mid; else hi = mid - 1;
   }
   return lo;
-}
-
-__device__ __forceinline__ bool clip_is_mine(const vp_clip_plan& pl, int variant, int64_t coff, int64_t pitch) {
-  return pl.status == VP_OK && pl.kernel_variant == variant && ((coff | pitch) & 15) == 0 && pl.tile_count > 0;
 }
 
 // Footprint of a strip: first pixel (16-aligned so that the byte offset 3*pa is 16-B aligned for TMA)
@@ -189,7 +188,6 @@ __device__ __forceinline__ void store_slots(void* pv, int64_t idx, float v0, flo
 // ---------------------------------------------------------------- configuration per variant
 template <int VARIANT>
 struct FastCfg {
-  static constexpr int LHM = VARIANT == KV_MILD ? 9 : (VARIANT == KV_MEDIUM ? 18 : 40);
   // union of two adjacent columns' windows: LHM + the largest start shift between them (<= ceil(fs)+1)
   static constexpr int UL = VARIANT == KV_MILD ? 11 : (VARIANT == KV_MEDIUM ? 23 : 51);
   static constexpr int MAXWS = kFastMaxWs;
@@ -215,7 +213,7 @@ struct ProdItem {
 };
 
 template <int VARIANT>
-__device__ __noinline__ ProdItem producer_open(const vp_clip_plan* __restrict__ plans, int n, int w,
+__device__ __noinline__ ProdItem producer_open(const vp_clip_plan* __restrict__ plans, const VIdx vx, int cnt, int w,
                                                const uint8_t* __restrict__ frames,
                                                const int64_t* __restrict__ clip_off,
                                                const int64_t* __restrict__ pitch_arr, int64_t item, int64_t my_b) {
@@ -225,18 +223,14 @@ __device__ __noinline__ ProdItem producer_open(const vp_clip_plan* __restrict__ 
   r.item = item;
   r.in_h = 0;
   r.nbytes = 0;
-  while (item < my_b) {
-    const int k = find_clip_f(plans, n, item);
+  if (item < my_b) {
+    const int j = vfind(vx, cnt, item);
+    const int k = vx.list[j];
     const vp_clip_plan pl = plans[k];
-    const int64_t cend = pl.tile_offset + pl.tile_count;
     const int64_t coff = clip_off[k], pitch = pitch_arr[k];
-    if (!clip_is_mine(pl, VARIANT, coff, pitch)) {
-      item = cend;
-      continue;
-    }
     const int ws = fast_strip_width(pl.in_w, pl.out_w);
     const int nstrips = (pl.out_w + ws - 1) / ws;
-    const int64_t local = item - pl.tile_offset;
+    const int64_t local = item - vx.off[j];
     const int f = (int)(local / nstrips), strip = (int)(local % nstrips);
     const Strip st = strip_of(pl, ws, strip);
     const int px0 = st.pa + w * kWarpPx;                       // this warp's first pixel
@@ -255,7 +249,7 @@ __device__ __noinline__ ProdItem producer_open(const vp_clip_plan* __restrict__ 
 
 template <int VARIANT, bool kF32>
 __global__ void __launch_bounds__(kNT, 2)
-resize_fast_kernel(FKParams kp, const vp_clip_plan* __restrict__ plans, int n, const uint8_t* __restrict__ frames,
+resize_fast_kernel(FKParams kp, const vp_clip_plan* __restrict__ plans, const VIdx vx, const uint8_t* __restrict__ frames,
                    const int64_t* __restrict__ clip_off, const int64_t* __restrict__ pitch_arr, void* pv_img,
                    int64_t img_cap, void* pv_vid, int64_t vid_cap) {
   using Cfg = FastCfg<VARIANT>;
@@ -278,12 +272,11 @@ resize_fast_kernel(FKParams kp, const vp_clip_plan* __restrict__ plans, int n, c
   int lane;
   asm volatile("mov.u32 %0, %%laneid;" : "=r"(lane));
 
-  // contiguous slice of the batch's fast-item space
-  const int64_t it_begin = plans[0].tile_offset;
-  const int64_t it_end = plans[n - 1].tile_offset + plans[n - 1].tile_count;
-  const int64_t total = it_end - it_begin;
-  const int64_t my_a = it_begin + total * blockIdx.x / gridDim.x;
-  const int64_t my_b = it_begin + total * (blockIdx.x + 1) / gridDim.x;
+  // contiguous slice of this variant's items
+  const int cnt = (int)vx.meta[0];
+  const int64_t total = vx.meta[1];
+  const int64_t my_a = total * blockIdx.x / gridDim.x;
+  const int64_t my_b = total * (blockIdx.x + 1) / gridDim.x;
 
   if (tid == 0) {
     for (int s = 0; s < kNVW * kNGrp; ++s) mbar_init(&full_all[s], 1);
@@ -311,7 +304,7 @@ resize_fast_kernel(FKParams kp, const vp_clip_plan* __restrict__ plans, int n, c
     auto issue = [&](uint32_t slot) {             // one row into staging slot `slot` (group barrier slot/4)
       if (prows == 0) {
         if (pit.src != nullptr || pit.item == my_a) {
-          pit = producer_open<VARIANT>(plans, n, warp, frames, clip_off, pitch_arr,
+          pit = producer_open<VARIANT>(plans, vx, cnt, warp, frames, clip_off, pitch_arr,
                                        pit.src != nullptr ? pit.item + 1 : my_a, my_b);
           if (pit.src == nullptr) pit.item = -1;       // exhausted
           psrc = pit.src;
@@ -335,13 +328,10 @@ resize_fast_kernel(FKParams kp, const vp_clip_plan* __restrict__ plans, int n, c
       for (uint32_t g = 0; g < kNGrp; ++g) issue_group(g);     // prefill
     int64_t item = my_a;
     while (item < my_b) {
-      const int k = find_clip_f(plans, n, item);
+      const int j = vfind(vx, cnt, item);
+      const int k = vx.list[j];
       const vp_clip_plan pl = plans[k];
-      const int64_t cend = pl.tile_offset + pl.tile_count;
-      if (!clip_is_mine(pl, VARIANT, clip_off[k], pitch_arr[k])) {
-        item = cend;
-        continue;
-      }
+      const int64_t cbase = vx.off[j], cend = vx.off[j + 1];
       const int ws = fast_strip_width(pl.in_w, pl.out_w);
       const int nstrips = (pl.out_w + ws - 1) / ws;
       const int in_h = pl.in_h, out_h = pl.out_h;
@@ -386,7 +376,7 @@ resize_fast_kernel(FKParams kp, const vp_clip_plan* __restrict__ plans, int n, c
         cached_clip = k;
       }
       for (; item < cend && item < my_b; ++item) {
-        const int64_t local = item - pl.tile_offset;
+        const int64_t local = item - cbase;
         const Strip st = strip_of(pl, ws, (int)(local % nstrips));
         const int px_lane = warp * kWarpPx + lane * 4;      // this lane's first pixel (relative to pa)
         const bool vactive = px_lane < st.np;
@@ -487,13 +477,10 @@ resize_fast_kernel(FKParams kp, const vp_clip_plan* __restrict__ plans, int n, c
   uint32_t vrow = 0;
   int64_t item = my_a;
   while (item < my_b) {
-    const int k = find_clip_f(plans, n, item);
+    const int j = vfind(vx, cnt, item);
+    const int k = vx.list[j];
     const vp_clip_plan pl = plans[k];
-    const int64_t cend = pl.tile_offset + pl.tile_count;
-    if (!clip_is_mine(pl, VARIANT, clip_off[k], pitch_arr[k])) {
-      item = cend;
-      continue;
-    }
+    const int64_t cbase = vx.off[j], cend = vx.off[j + 1];
     void* pv = pl.is_image ? pv_img : pv_vid;
     const int64_t cap = pl.is_image ? img_cap : vid_cap;
     const bool writable = pv != nullptr && pl.patch_offset + (int64_t)pl.grid_t * pl.grid_h * pl.grid_w <= cap;
@@ -501,7 +488,7 @@ resize_fast_kernel(FKParams kp, const vp_clip_plan* __restrict__ plans, int n, c
     const int nstrips = (pl.out_w + ws - 1) / ws;
     const int out_h = pl.out_h;
     for (; item < cend && item < my_b; ++item) {
-      const int64_t local = item - pl.tile_offset;
+      const int64_t local = item - cbase;
       const int f = (int)(local / nstrips);
       const Strip st = strip_of(pl, ws, (int)(local % nstrips));
       // ---- horizontal weights of this strip: per column pair (ja, ja+1) the union of the two windows
@@ -642,12 +629,200 @@ resize_fast_kernel(FKParams kp, const vp_clip_plan* __restrict__ plans, int n, c
   }
 }
 
+
+// ---------------------------------------------------------------- KV_COPY (identity resize)
+// Item = (clip, frame f, merge-row band hb, chunk wc of kCopyMW merge columns).  The band's B = m*p source
+// rows x (<= kCopyMW*B) pixels are staged in shared memory with 16-B loads; each thread then owns fixed
+// (channel, element-pair) positions of a patch's p x p chunk and walks the item's patches, writing
+// bf16x2 / float2 pairs -- consecutive threads write consecutive elements of one chunk (coalesced).
+// Numerics equal the fast kernel's on an identity axis pair (weights exactly 1): x*scale+bias, clamp
+// in the output domain.
+constexpr int kCT = 256;
+
+template <bool kF32>
+__global__ void __launch_bounds__(kCT)
+resize_copy_kernel(FKParams kp, const vp_clip_plan* __restrict__ plans, const VIdx vx, const uint8_t* __restrict__ frames,
+                   const int64_t* __restrict__ clip_off, const int64_t* __restrict__ pitch_arr, void* pv_img,
+                   int64_t img_cap, void* pv_vid, int64_t vid_cap) {
+  extern __shared__ __align__(16) unsigned char csm[];
+  const int tid = threadIdx.x;
+  const int p = kp.p, m = kp.m, tp = kp.tp, B = m * p, pp = p * p, half_pp = pp / 2;
+  // contiguous slice of this variant's items
+  const int cnt = (int)vx.meta[0];
+  const int64_t total = vx.meta[1];
+  const int64_t my_a = total * blockIdx.x / gridDim.x;
+  const int64_t my_b = total * (blockIdx.x + 1) / gridDim.x;
+  constexpr int kMaxW = 2;                          // element pairs per thread per pass over a patch
+  const int npos = 3 * half_pp;                     // (channel, element pair) positions of one patch
+  int64_t item = my_a;
+  while (item < my_b) {
+    const int j = vfind(vx, cnt, item);
+    const int k = vx.list[j];
+    const vp_clip_plan pl = plans[k];
+    const int64_t cbase = vx.off[j], cend = vx.off[j + 1];
+    const int64_t coff = clip_off[k], pitch = pitch_arr[k];
+    void* pv = pl.is_image ? pv_img : pv_vid;
+    const int64_t cap = pl.is_image ? img_cap : vid_cap;
+    const bool writable = pv != nullptr && pl.patch_offset + (int64_t)pl.grid_t * pl.grid_h * pl.grid_w <= cap;
+    const int gh = pl.grid_h, gw = pl.grid_w, nwc = copy_wchunks(gw, m), nhb = gh / m;
+    const int64_t group_stride = (int64_t)nhb * (gw / m) * m * m * kp.D;
+    for (; item < cend && item < my_b; ++item) {
+      const int64_t local = item - cbase;
+      const int f = (int)(local / ((int64_t)nhb * nwc));
+      const int rem = (int)(local - (int64_t)f * nhb * nwc);
+      const int hb = rem / nwc, wc = rem - hb * nwc;
+      const int mc0 = wc * kCopyMW, nmc = min(kCopyMW, gw / m - mc0);   // merge columns of this item
+      const int x0 = mc0 * B, ncols = nmc * B;
+      const int rb = (3 * ncols + 15) & ~15;                           // staged row bytes (16-B multiple)
+      const uint8_t* src = frames + coff + ((int64_t)f * pl.in_h + (int64_t)hb * B) * pitch + 3 * (int64_t)x0;
+      __syncthreads();                                                 // previous item's readers are done
+      const int q16 = rb >> 4;
+      for (int i = tid; i < B * q16; i += kCT) {
+        const int r = i / q16, q = i - r * q16;
+        reinterpret_cast<uint4*>(csm + r * rb)[q] = __ldg(reinterpret_cast<const uint4*>(src + r * pitch) + q);
+      }
+      __syncthreads();
+      if (!writable) continue;
+      const int last_slot = (f == pl.n_frames - 1) ? pl.grid_t * tp - 1 : f;   // O7: frame n-1 fills pads
+      const int nslots = last_slot - f + 1;
+      const int g0 = f / tp, ti0 = f - g0 * tp;
+      // patch row of (merge column mc, mh, mw) in slot group g0: patch_offset + ((g0*nhb + hb)*(gw/m) + mc)*m^2 + mh*m + mw
+      const int64_t band_row = pl.patch_offset + ((int64_t)g0 * nhb + hb) * (gw / m) * m * m;
+      const int npatch = nmc * m * m;
+      for (int wb = 0; wb < npos; wb += kCT * kMaxW) {
+        // this thread's fixed (channel, element pair) positions: w = c * pp/2 + e2
+        int woff[kMaxW], wsrc[kMaxW];
+        float wsc[kMaxW], wbi[kMaxW], wlo[kMaxW], whi[kMaxW];
+        __nv_bfloat162 wlo2[kMaxW], whi2[kMaxW];
+        bool wv[kMaxW];
+#pragma unroll
+        for (int t = 0; t < kMaxW; ++t) {
+          const int w = wb + tid + t * kCT;
+          wv[t] = w < npos;
+          const int c = wv[t] ? w / half_pp : 0, e = wv[t] ? 2 * (w - c * half_pp) : 0;
+          const int py = e / p, px = e - py * p;
+          woff[t] = c * tp * pp + e + ti0 * pp;       // element offset inside the patch row (first slot)
+          wsrc[t] = py * rb + 3 * px + c;             // staged byte offset inside the patch
+          // per-channel constants selected without dynamic indexing of the parameter arrays
+          wsc[t] = c == 0 ? kp.scale[0] : (c == 1 ? kp.scale[1] : kp.scale[2]);
+          wbi[t] = c == 0 ? kp.bias[0] : (c == 1 ? kp.bias[1] : kp.bias[2]);
+          wlo[t] = c == 0 ? kp.lo[0] : (c == 1 ? kp.lo[1] : kp.lo[2]);
+          whi[t] = c == 0 ? kp.hi[0] : (c == 1 ? kp.hi[1] : kp.hi[2]);
+          wlo2[t] = c == 0 ? kp.lo2[0] : (c == 1 ? kp.lo2[1] : kp.lo2[2]);
+          whi2[t] = c == 0 ? kp.hi2[0] : (c == 1 ? kp.hi2[1] : kp.hi2[2]);
+        }
+        for (int pi = 0; pi < npatch; ++pi) {
+          const int j = pi / (m * m), r2 = pi - j * m * m, mh = r2 / m, mw = r2 - mh * m;
+          const int64_t prow = band_row + (int64_t)(mc0 + j) * m * m + r2;
+          const uint8_t* sp = csm + (mh * p) * rb + 3 * (j * B + mw * p);
+#pragma unroll
+          for (int t = 0; t < kMaxW; ++t) {
+            if (!wv[t]) continue;
+            const uint8_t* s2 = sp + wsrc[t];
+            const float v0 = fmaf((float)s2[0], wsc[t], wbi[t]);
+            const float v1 = fmaf((float)s2[3], wsc[t], wbi[t]);
+            int64_t idx = prow * kp.D + woff[t];
+            if (kF32) {
+              const float2 o = make_float2(fminf(fmaxf(v0, wlo[t]), whi[t]), fminf(fmaxf(v1, wlo[t]), whi[t]));
+              for (int s2i = 0, ti = ti0; s2i < nslots; ++s2i) {
+                *reinterpret_cast<float2*>(reinterpret_cast<float*>(pv) + idx) = o;
+                if (++ti == tp) { ti = 0; idx += group_stride - (int64_t)(tp - 1) * pp; } else idx += pp;
+              }
+            } else {
+              const __nv_bfloat162 o = __hmin2(__hmax2(__floats2bfloat162_rn(v0, v1), wlo2[t]), whi2[t]);
+              for (int s2i = 0, ti = ti0; s2i < nslots; ++s2i) {
+                *reinterpret_cast<__nv_bfloat162*>(reinterpret_cast<__nv_bfloat16*>(pv) + idx) = o;
+                if (++ti == tp) { ti = 0; idx += group_stride - (int64_t)(tp - 1) * pp; } else idx += pp;
+              }
+            }
+          }
+        }
+      }
+    }
+  }
+}
+
 int g_num_sms = 0;
 bool g_attr[3][2] = {};
+bool g_cattr[2] = {};
+
+// ---------------------------------------------------------------- per-variant work index
+// One CTA: slot v in {MILD, MEDIUM, STRONG, COPY} collects the valid, 16-B aligned clips of that variant
+// (list, batch order) and the exclusive prefix of their item counts (off); meta[v] = {count, items}.
+constexpr int kNSlots = 4;
+constexpr int kIdxThreads = 1024;
+__device__ __forceinline__ int variant_slot(int kv) { return kv == KV_COPY ? 3 : (kv <= KV_STRONG ? kv : -1); }
+
+__global__ void __launch_bounds__(kIdxThreads)
+variant_index_kernel(const vp_clip_plan* __restrict__ plans, int n, const int64_t* __restrict__ coff,
+                     const int64_t* __restrict__ pitch, int* __restrict__ list, int64_t* __restrict__ off,
+                     int64_t* __restrict__ meta) {
+  __shared__ int64_t wsum[kIdxThreads / 32][kNSlots];
+  __shared__ int wcnt[kIdxThreads / 32][kNSlots];
+  __shared__ int64_t c_items[kNSlots];
+  __shared__ int c_cnt[kNSlots];
+  const int tid = threadIdx.x, lane = tid & 31, warp = tid >> 5;
+  if (tid < kNSlots) { c_items[tid] = 0; c_cnt[tid] = 0; }
+  __syncthreads();
+  for (int c0 = 0; c0 < n; c0 += kIdxThreads) {
+    const int k = c0 + tid;
+    int slot = -1;
+    int64_t items = 0;
+    if (k < n) {
+      const vp_clip_plan& pl = plans[k];
+      if (pl.status == VP_OK && pl.tile_count > 0 && ((coff[k] | pitch[k]) & 15) == 0) {
+        slot = variant_slot(pl.kernel_variant);
+        items = pl.tile_count;
+      }
+    }
+    int64_t ex_items = 0;
+    int ex_cnt = 0;
+#pragma unroll
+    for (int v = 0; v < kNSlots; ++v) {
+      int64_t x = slot == v ? items : 0;
+      int y = slot == v ? 1 : 0;
+#pragma unroll
+      for (int o = 1; o < 32; o <<= 1) {
+        const int64_t xa = __shfl_up_sync(0xffffffffu, x, o);
+        const int ya = __shfl_up_sync(0xffffffffu, y, o);
+        if (lane >= o) { x += xa; y += ya; }
+      }
+      if (lane == 31) { wsum[warp][v] = x; wcnt[warp][v] = y; }
+      if (slot == v) { ex_items = x - items; ex_cnt = y - 1; }
+    }
+    __syncthreads();
+    int64_t add_items = 0, tot_items[kNSlots];
+    int add_cnt = 0, tot_cnt[kNSlots];
+#pragma unroll
+    for (int v = 0; v < kNSlots; ++v) { tot_items[v] = 0; tot_cnt[v] = 0; }
+    for (int w = 0; w < kIdxThreads / 32; ++w) {
+#pragma unroll
+      for (int v = 0; v < kNSlots; ++v) {
+        if (w < warp && slot == v) { add_items += wsum[w][v]; add_cnt += wcnt[w][v]; }
+        tot_items[v] += wsum[w][v];
+        tot_cnt[v] += wcnt[w][v];
+      }
+    }
+    if (slot >= 0) {
+      const int pos = c_cnt[slot] + add_cnt + ex_cnt;
+      list[(size_t)slot * n + pos] = k;
+      off[(size_t)slot * (n + 1) + pos] = c_items[slot] + add_items + ex_items;
+    }
+    __syncthreads();
+    if (tid < kNSlots) { c_items[tid] += tot_items[tid]; c_cnt[tid] += tot_cnt[tid]; }
+    __syncthreads();
+  }
+  if (tid < kNSlots) {
+    off[(size_t)tid * (n + 1) + c_cnt[tid]] = c_items[tid];
+    meta[2 * tid] = c_cnt[tid];
+    meta[2 * tid + 1] = c_items[tid];
+  }
+}
 
 template <int VARIANT, bool kF32>
-void launch_fast(const FKParams& kp, const vp_clip_plan* plans, int n, const uint8_t* frames, const int64_t* coff,
-                 const int64_t* pitch, void* pi, int64_t icap, void* pvv, int64_t vcap, cudaStream_t s) {
+void launch_fast(const FKParams& kp, const vp_clip_plan* plans, const VIdx& vx, const uint8_t* frames,
+                 const int64_t* coff, const int64_t* pitch, void* pi, int64_t icap, void* pvv, int64_t vcap,
+                 cudaStream_t s) {
   using Cfg = FastCfg<VARIANT>;
   auto kern = resize_fast_kernel<VARIANT, kF32>;
   if (!g_attr[VARIANT][kF32]) {
@@ -657,15 +832,33 @@ void launch_fast(const FKParams& kp, const vp_clip_plan* plans, int n, const uin
   int per_sm = 0;
   cudaOccupancyMaxActiveBlocksPerMultiprocessor(&per_sm, kern, kNT, Cfg::SMEM);
   if (per_sm < 1) per_sm = 1;
-  kern<<<g_num_sms * per_sm, kNT, Cfg::SMEM, s>>>(kp, plans, n, frames, coff, pitch, pi, icap, pvv, vcap);
+  kern<<<g_num_sms * per_sm, kNT, Cfg::SMEM, s>>>(kp, plans, vx, frames, coff, pitch, pi, icap, pvv, vcap);
+}
+
+template <bool kF32>
+void launch_copy(const FKParams& kp, const vp_clip_plan* plans, const VIdx& vx, const uint8_t* frames,
+                 const int64_t* coff, const int64_t* pitch, void* pi, int64_t icap, void* pvv, int64_t vcap,
+                 cudaStream_t s) {
+  auto kern = resize_copy_kernel<kF32>;
+  const int B = kp.m * kp.p;
+  const size_t smem = (size_t)B * ((3 * kCopyMW * B + 15) & ~15);
+  if (!g_cattr[kF32]) {
+    cudaFuncSetAttribute(kern, cudaFuncAttributeMaxDynamicSharedMemorySize, 200 * 1024);
+    g_cattr[kF32] = true;
+  }
+  int per_sm = 0;
+  cudaOccupancyMaxActiveBlocksPerMultiprocessor(&per_sm, kern, kCT, smem);
+  if (per_sm < 1) per_sm = 1;
+  kern<<<g_num_sms * per_sm, kCT, smem, s>>>(kp, plans, vx, frames, coff, pitch, pi, icap, pvv, vcap);
 }
 
 }  // namespace
 
-// Launch the fast variants (each skips clips that are not its own).
-void launch_resize_fast(const vp_params* p, const vp_clip_plan* plans, int n, const uint8_t* frames,
-                        const int64_t* coff, const int64_t* pitch, void* pi, int64_t icap, void* pvv, int64_t vcap,
-                        cudaStream_t s) {
+// Launch the fast variants: build the per-variant work index in stream-ordered scratch, then one launch
+// per variant (each spreads its own items over the whole GPU).
+cudaError_t launch_resize_fast(const vp_params* p, const vp_clip_plan* plans, int n, const uint8_t* frames,
+                               const int64_t* coff, const int64_t* pitch, void* pi, int64_t icap, void* pvv,
+                               int64_t vcap, cudaStream_t s) {
   if (g_num_sms == 0) {
     int dev = 0;
     cudaGetDevice(&dev);
@@ -685,15 +878,46 @@ void launch_resize_fast(const vp_params* p, const vp_clip_plan* plans, int n, co
     kp.lo2[c] = __floats2bfloat162_rn(kp.lo[c], kp.lo[c]);
     kp.hi2[c] = __floats2bfloat162_rn(kp.hi[c], kp.hi[c]);
   }
-  if (p->out_dtype == VP_OUT_F32) {
-    launch_fast<KV_MILD, true>(kp, plans, n, frames, coff, pitch, pi, icap, pvv, vcap, s);
-    launch_fast<KV_MEDIUM, true>(kp, plans, n, frames, coff, pitch, pi, icap, pvv, vcap, s);
-    launch_fast<KV_STRONG, true>(kp, plans, n, frames, coff, pitch, pi, icap, pvv, vcap, s);
-  } else {
-    launch_fast<KV_MILD, false>(kp, plans, n, frames, coff, pitch, pi, icap, pvv, vcap, s);
-    launch_fast<KV_MEDIUM, false>(kp, plans, n, frames, coff, pitch, pi, icap, pvv, vcap, s);
-    launch_fast<KV_STRONG, false>(kp, plans, n, frames, coff, pitch, pi, icap, pvv, vcap, s);
+  const size_t list_b = ((size_t)kNSlots * n * sizeof(int) + 15) & ~(size_t)15;
+  const size_t off_b = (size_t)kNSlots * (n + 1) * sizeof(int64_t);
+  const size_t bytes = list_b + off_b + 2 * kNSlots * sizeof(int64_t);
+  // library-owned stream-ordered pool that keeps its memory between calls (release threshold = max), so
+  // the per-call scratch is a pool hit, not a driver allocation; the process's default pool is untouched
+  static cudaMemPool_t pool = nullptr;
+  static int pool_dev = -1;
+  int dev = 0;
+  cudaGetDevice(&dev);
+  if (pool == nullptr || pool_dev != dev) {
+    cudaMemPoolProps props{};
+    props.allocType = cudaMemAllocationTypePinned;
+    props.location.type = cudaMemLocationTypeDevice;
+    props.location.id = dev;
+    cudaError_t pe = cudaMemPoolCreate(&pool, &props);
+    if (pe != cudaSuccess) return pe;
+    uint64_t thr = ~0ull;
+    cudaMemPoolSetAttribute(pool, cudaMemPoolAttrReleaseThreshold, &thr);
+    pool_dev = dev;
   }
+  void* scratch = nullptr;
+  cudaError_t e = cudaMallocFromPoolAsync(&scratch, bytes, pool, s);
+  if (e != cudaSuccess) return e;
+  int* list = reinterpret_cast<int*>(scratch);
+  int64_t* off = reinterpret_cast<int64_t*>(reinterpret_cast<char*>(scratch) + list_b);
+  int64_t* meta = off + (size_t)kNSlots * (n + 1);
+  variant_index_kernel<<<1, kIdxThreads, 0, s>>>(plans, n, coff, pitch, list, off, meta);
+  auto vx = [&](int slot) { return VIdx{list + (size_t)slot * n, off + (size_t)slot * (n + 1), meta + 2 * slot}; };
+  if (p->out_dtype == VP_OUT_F32) {
+    launch_fast<KV_MILD, true>(kp, plans, vx(0), frames, coff, pitch, pi, icap, pvv, vcap, s);
+    launch_fast<KV_MEDIUM, true>(kp, plans, vx(1), frames, coff, pitch, pi, icap, pvv, vcap, s);
+    launch_fast<KV_STRONG, true>(kp, plans, vx(2), frames, coff, pitch, pi, icap, pvv, vcap, s);
+    launch_copy<true>(kp, plans, vx(3), frames, coff, pitch, pi, icap, pvv, vcap, s);
+  } else {
+    launch_fast<KV_MILD, false>(kp, plans, vx(0), frames, coff, pitch, pi, icap, pvv, vcap, s);
+    launch_fast<KV_MEDIUM, false>(kp, plans, vx(1), frames, coff, pitch, pi, icap, pvv, vcap, s);
+    launch_fast<KV_STRONG, false>(kp, plans, vx(2), frames, coff, pitch, pi, icap, pvv, vcap, s);
+    launch_copy<false>(kp, plans, vx(3), frames, coff, pitch, pi, icap, pvv, vcap, s);
+  }
+  return cudaFreeAsync(scratch, s);
 }
 
 }  // namespace vp

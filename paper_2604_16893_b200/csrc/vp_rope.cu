@@ -166,7 +166,6 @@ rope_fill_kernel(const int8_t* __restrict__ tt, const int64_t* __restrict__ cu, 
                  const double* __restrict__ spg, int tps, const int64_t* __restrict__ counts,
                  const int64_t* __restrict__ vcum, int64_t* __restrict__ pos, int64_t total_L,
                  int64_t* __restrict__ deltas, int32_t* __restrict__ status) {
-  __shared__ int64_t sh3[kWarps][3];
   __shared__ int64_t sh2[kWarps][2];
   __shared__ int64_t shm[kWarps];
   __shared__ int s_bad, s_vlo, s_vhi;

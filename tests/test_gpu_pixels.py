@@ -93,6 +93,22 @@ def test_mild_upscale_and_identity_edges(dtype):
     _full_compare(pre, clips)
 
 
+@pytest.mark.parametrize("dtype", [1, 0])
+@pytest.mark.parametrize("patch,tp", [(14, 3), (16, 2), (16, 1)])
+def test_identity_copy_variant(dtype, patch, tp):
+    """Both axes identity (KV_COPY): ragged merge-column chunks (gw/m = 11, 19), odd tp with temporal
+    padding, images filling tp slots, a 1-frame video, and p = 14 (28-byte patch rows)."""
+    import paper_2604_16893_b200 as vp
+    f = 2 * patch
+    pre = vp.VisualPreprocessor(patch_size=patch, temporal_patch_size=tp, max_frames=max(tp, 5),
+                                image_max_pixels=f * f * 400, video_max_pixels=f * f * 400, out_dtype=dtype)
+    clips = [I.image(2 * f, 11 * f), I.clip(5, 2.0, 3 * f, 19 * f), I.image(f, f), I.clip(1, 1.0, f, 2 * f),
+             I.image(7 * f, 3 * f)]
+    pl = pre.plan(clips)
+    assert all(v == 4 for v in pl.plans_host["kernel_variant"][:len(clips)]), pl.plans_host["kernel_variant"]
+    _full_compare(pre, clips)
+
+
 def test_cfg2_one_clip_full():
     """BASELINE cfg2 at full size, compared element by element (64 frames 720p -> 384x672)."""
     import paper_2604_16893_b200 as vp
