@@ -49,7 +49,7 @@ PLAN_DTYPE = np.dtype([("status", "<i4"), ("is_image", "<i4"), ("in_h", "<i4"), 
 
 def _load() -> C.CDLL:
     if not os.path.exists(LIB_PATH):
-        raise ImportError(f"{LIB_PATH} is missing: build it with `python -m paper_2604_16893_b200._build` "
+        raise ImportError(f"{LIB_PATH} is missing: build it with `python paper_2604_16893_b200/_build.py` "
                           f"(or __graft_entry__.build()); there is no CPU fallback")
     lib = C.CDLL(LIB_PATH)
     vp = C.c_void_p

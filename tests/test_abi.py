@@ -23,7 +23,11 @@ def test_header_declares_the_north_star_calls():
 
 
 def test_library_exports_every_declared_symbol():
-    from paper_2604_16893_b200 import _build
+    # Load _build.py by path: importing the package needs the library it builds.
+    import importlib.util
+    spec = importlib.util.spec_from_file_location("_vp_build", os.path.join(ROOT, "paper_2604_16893_b200", "_build.py"))
+    _build = importlib.util.module_from_spec(spec)
+    spec.loader.exec_module(_build)
     lib = C.CDLL(_build.build())
     for s in _declared_symbols():
         assert hasattr(lib, s), s
