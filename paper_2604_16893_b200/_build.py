@@ -12,7 +12,7 @@ LIB = os.path.join(HERE, "libvp.so")
 ARCH = ["-gencode", "arch=compute_100a,code=sm_100a"]
 # vp_plan.cu carries the bit-exact f64 planning: no FMA contraction there (SURVEY §7 hard parts).
 PER_FILE = {"vp_plan.cu": ["--fmad=false"]}
-SOURCES = ["vp_abi.cu", "vp_plan.cu", "vp_resize.cu", "vp_resize_fast.cu", "vp_rope.cu", "vp_synth.cu"]
+SOURCES = ["vp_abi.cu", "vp_plan.cu", "vp_resize.cu", "vp_resize_fast.cu", "vp_resize_ring.cu", "vp_rope.cu", "vp_synth.cu"]
 
 
 def nvcc() -> str:
@@ -24,7 +24,7 @@ def nvcc() -> str:
 
 def build(verbose: bool = False, force: bool = False) -> str:
     srcs = [os.path.join(CSRC, s) for s in SOURCES]
-    deps = srcs + [os.path.join(CSRC, "vp_internal.cuh"), os.path.join(HERE, "..", "include", "vp.h"), __file__]
+    deps = srcs + [os.path.join(CSRC, "vp_internal.cuh"), os.path.join(CSRC, "vp_k3_common.cuh"), os.path.join(HERE, "..", "include", "vp.h"), __file__]
     if not force and os.path.exists(LIB) and all(os.path.getmtime(LIB) >= os.path.getmtime(d) for d in deps):
         return LIB
     objdir = os.path.join(HERE, "build")

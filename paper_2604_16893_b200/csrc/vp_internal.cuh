@@ -50,7 +50,7 @@ constexpr int kTotLen = VP_TOT_LEN;
 // KV_GENERIC covers everything else (vp_resize.cu, token tiles).  A clip's items (tile_count)
 // are n_frames x n_strips for the fast variants, 0 for generic.  Integer / f64 exact.
 // ------------------------------------------------------------------------------------------
-enum { KV_MILD = 0, KV_MEDIUM = 1, KV_STRONG = 2, KV_GENERIC = 3, KV_COPY = 4 };
+enum { KV_MILD = 0, KV_MEDIUM = 1, KV_STRONG = 2, KV_GENERIC = 3, KV_COPY = 4, KV_RING = 5 };
 constexpr int kRing = 5;          // vertical ring slots: max live output rows per source row for in/out > 0.8
 constexpr int kInHMax = 1088;     // source rows supported by the fast kernel's per-row weight table
 constexpr int kWListMax = 6144;   // vertical weights (sum of window lengths) held in smem
@@ -97,8 +97,31 @@ __host__ __device__ __forceinline__ int fast_strip_width(int in_w, int out_w) {
 constexpr int kCopyMW = 8;
 __host__ __device__ __forceinline__ int copy_wchunks(int grid_w, int m) { return (grid_w / m + kCopyMW - 1) / kCopyMW; }
 
-__host__ __device__ __forceinline__ int select_variant(int in_h, int in_w, int out_h, int out_w, int p) {
+// KV_RING (vp_resize_ring.cu): one warp per CTA streams a (clip, strip, frame) item through a vertical
+// register ring (lanes = 4 source pixels, <= kRingPx footprint pixels per strip) and a horizontal ring
+// (lanes = output rows).  Both axes must be downscales or identity (in >= out): then at most 5 output rows
+// (columns) are live per source row (pixel), see DESIGN.md.  The strip width is the largest multiple of 8
+// whose footprint, started at a 4-pixel boundary, fits kRingPx:  3 + (Ws-1)*s + 2*(2*fs) + 2 <= kRingPx.
+// Strips narrower than kRingMinWs would re-read too much halo; those clips use the other variants.
+constexpr int kRingPx = 120;      // 30 lanes x 4 px
+constexpr int kRingMaxWs = 64;
+constexpr int kRingMinWs = 32;
+constexpr int kRingInHMax = 2176; // per-clip vertical table rows (ring_vtables_kernel slot size)
+__host__ __device__ __forceinline__ int ring_strip_width(int in_w, int out_w) {
+  if (in_w < out_w) return 0;
+  const double s = (double)in_w / (double)out_w;
+  int best = 0;
+  for (int ws = 8; ws <= kRingMaxWs; ws += 8)
+    if (3.0 + (ws - 1) * s + 4.0 * s + 2.0 <= (double)kRingPx) best = ws;
+  if (best > out_w) best = out_w;
+  return best;
+}
+
+__host__ __device__ __forceinline__ int select_variant(int in_h, int in_w, int out_h, int out_w, int p, int ring) {
   if (in_h == out_h && in_w == out_w && (p & 1) == 0) return KV_COPY;
+  if (ring && in_h >= out_h && in_h <= kRingInHMax && p == 16 && ring_strip_width(in_w, out_w) >= kRingMinWs &&
+      out_w % 8 == 0)
+    return KV_RING;
   const double sv = (double)in_h / (double)out_h;
   // live output rows per source row <= floor(4/s)+1 for upscale (<= 5 iff s > 0.8) and <= 5 for downscale
   // (trimmed windows; brute-forced in tests/test_oracle_pixels.py::test_live_rows_bound)

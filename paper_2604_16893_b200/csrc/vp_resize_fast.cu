@@ -20,8 +20,7 @@
 // of the weights of its live output rows + the live count (fp32 from f64); windows are trimmed of
 // exact-zero taps (identity axes become 1-tap copies).  Per item: the strip's horizontal weights.
 // The V warps load row y+1's staged bytes and weight vector while FMA-ing row y (software pipeline).
-#include "vp_internal.cuh"
-#include <cuda_bf16.h>
+#include "vp_k3_common.cuh"
 
 namespace vp {
 namespace {
@@ -37,94 +36,6 @@ constexpr int kWarpB = 3 * kWarpPx;       // 384 bytes
 constexpr int kCapR = 4;                  // retired-row buffer rows (V -> H)
 constexpr int kRowPx = kFastPx + 48;      // float4 pixels per buffered row (+ tap slack)
 
-struct FKParams {
-  int p, m, tp, D;
-  float scale[3], bias[3];
-  float lo[3], hi[3];               // output-domain clamp bounds: bias, fma(255, scale, bias)
-  __nv_bfloat162 lo2[3], hi2[3];    // the same, RNE to bf16, duplicated
-};
-
-// ---------------------------------------------------------------- PTX helpers (mbarrier / TMA bulk)
-__device__ __forceinline__ uint32_t smem_u32(const void* p) {
-  return static_cast<uint32_t>(__cvta_generic_to_shared(p));
-}
-__device__ __forceinline__ void mbar_init(uint64_t* bar, uint32_t count) {
-  asm volatile("mbarrier.init.shared::cta.b64 [%0], %1;" ::"r"(smem_u32(bar)), "r"(count));
-}
-__device__ __forceinline__ void mbar_expect_tx(uint64_t* bar, uint32_t bytes) {
-  asm volatile("mbarrier.expect_tx.relaxed.cta.shared::cta.b64 [%0], %1;" ::"r"(smem_u32(bar)), "r"(bytes) : "memory");
-}
-__device__ __forceinline__ void mbar_arrive(uint64_t* bar) {
-  asm volatile("mbarrier.arrive.release.cta.shared::cta.b64 _, [%0];" ::"r"(smem_u32(bar)) : "memory");
-}
-__device__ __forceinline__ void mbar_wait(uint64_t* bar, uint32_t parity) {
-  asm volatile(
-      "{\n"
-      ".reg .pred P1;\n"
-      "WAIT_%=:\n"
-      "mbarrier.try_wait.parity.acquire.cta.shared::cta.b64 P1, [%0], %1;\n"
-      "@!P1 bra WAIT_%=;\n"
-      "}\n" ::"r"(smem_u32(bar)),
-      "r"(parity)
-      : "memory");
-}
-__device__ __forceinline__ void tma_bulk_g2s(void* dst, const void* src, uint32_t bytes, uint64_t* bar) {
-  asm volatile(
-      "cp.async.bulk.shared::cluster.global.mbarrier::complete_tx::bytes [%0], [%1], %2, [%3];" ::"r"(
-          smem_u32(dst)),
-      "l"(src), "r"(bytes), "r"(smem_u32(bar))
-      : "memory");
-}
-__device__ __forceinline__ void named_sync(int id, int nthreads) {
-  asm volatile("bar.sync %0, %1;" ::"r"(id), "r"(nthreads) : "memory");
-}
-
-__device__ __forceinline__ double keys_d(double x) {
-  const double a = -0.5;
-  x = fabs(x);
-  if (x < 1.0) return ((a + 2.0) * x - (a + 3.0)) * x * x + 1.0;
-  if (x < 2.0) return (((x - 5.0) * x + 8.0) * x - 4.0) * a;
-  return 0.0;
-}
-
-// Window of output index i on an in->out axis (C10), trimmed of exact-zero end taps (zero taps add
-// exactly 0 to the sum; trimming makes identity axes 1-tap).  x0, x1 (exclusive), centre c, 1/fs.
-struct Win {
-  int x0, x1;
-  double c, inv;
-};
-__device__ __forceinline__ Win window_of(int in, int out, int i) {
-  const double scale = (double)in / (double)out;
-  const double fs = scale > 1.0 ? scale : 1.0;
-  const double support = 2.0 * fs;
-  Win w;
-  w.inv = 1.0 / fs;
-  w.c = ((double)i + 0.5) * scale;
-  w.x0 = (int)(w.c - support + 0.5);
-  if (w.x0 < 0) w.x0 = 0;
-  w.x1 = (int)(w.c + support + 0.5);
-  if (w.x1 > in) w.x1 = in;
-  while (w.x1 - w.x0 > 1 && keys_d(((double)w.x0 - w.c + 0.5) * w.inv) == 0.0) ++w.x0;
-  while (w.x1 - w.x0 > 1 && keys_d(((double)(w.x1 - 1) - w.c + 0.5) * w.inv) == 0.0) --w.x1;
-  return w;
-}
-
-// Per-variant work index (built per call by variant_index_kernel): the variant's clips in batch order
-// (list), the exclusive prefix of their item counts (off, count+1 entries) and meta = {count, items}.
-// Every CTA of a variant's launch takes a contiguous slice of that variant's items only.
-struct VIdx {
-  const int* list;
-  const int64_t* off;
-  const int64_t* meta;
-};
-__device__ __forceinline__ int vfind(const VIdx& vx, int cnt, int64_t item) {   // last j with off[j] <= item
-  int lo = 0, hi = cnt - 1;
-  while (lo < hi) {
-    const int mid = (lo + hi + 1) >> 1;
-    if (vx.off[mid] <= item) lo = mid; else hi = mid - 1;
-  }
-  return lo;
-}
 
 // Footprint of a strip: first pixel (16-aligned so that the byte offset 3*pa is 16-B aligned for TMA)
 // and pixel count.
@@ -749,9 +660,10 @@ bool g_cattr[2] = {};
 // ---------------------------------------------------------------- per-variant work index
 // One CTA: slot v in {MILD, MEDIUM, STRONG, COPY} collects the valid, 16-B aligned clips of that variant
 // (list, batch order) and the exclusive prefix of their item counts (off); meta[v] = {count, items}.
-constexpr int kNSlots = 4;
 constexpr int kIdxThreads = 1024;
-__device__ __forceinline__ int variant_slot(int kv) { return kv == KV_COPY ? 3 : (kv <= KV_STRONG ? kv : -1); }
+__device__ __forceinline__ int variant_slot(int kv) {
+  return kv == KV_COPY ? 3 : (kv == KV_RING ? 4 : (kv <= KV_STRONG ? kv : -1));
+}
 
 __global__ void __launch_bounds__(kIdxThreads)
 variant_index_kernel(const vp_clip_plan* __restrict__ plans, int n, const int64_t* __restrict__ coff,
@@ -870,6 +782,7 @@ cudaError_t launch_resize_fast(const vp_params* p, const vp_clip_plan* plans, in
   kp.m = p->merge_size;
   kp.tp = p->temporal_patch_size;
   kp.D = 3 * kp.tp * kp.p * kp.p;
+  kp.out_f32 = p->out_dtype == VP_OUT_F32;
   for (int c = 0; c < 3; ++c) {
     kp.scale[c] = (float)(1.0 / (255.0 * p->std[c]));
     kp.bias[c] = (float)(-p->mean[c] / p->std[c]);
@@ -880,7 +793,10 @@ cudaError_t launch_resize_fast(const vp_params* p, const vp_clip_plan* plans, in
   }
   const size_t list_b = ((size_t)kNSlots * n * sizeof(int) + 15) & ~(size_t)15;
   const size_t off_b = (size_t)kNSlots * (n + 1) * sizeof(int64_t);
-  const size_t bytes = list_b + off_b + 2 * kNSlots * sizeof(int64_t);
+  const size_t meta_b = 2 * kNSlots * sizeof(int64_t);
+  const size_t own_b = ((size_t)n * sizeof(int) + 255) & ~(size_t)255;
+  const size_t vt_off = (list_b + off_b + meta_b + own_b + 255) & ~(size_t)255;
+  const size_t bytes = vt_off + (size_t)n * ring_vtable_bytes();
   // library-owned stream-ordered pool that keeps its memory between calls (release threshold = max), so
   // the per-call scratch is a pool hit, not a driver allocation; the process's default pool is untouched
   static cudaMemPool_t pool = nullptr;
@@ -904,6 +820,8 @@ cudaError_t launch_resize_fast(const vp_params* p, const vp_clip_plan* plans, in
   int* list = reinterpret_cast<int*>(scratch);
   int64_t* off = reinterpret_cast<int64_t*>(reinterpret_cast<char*>(scratch) + list_b);
   int64_t* meta = off + (size_t)kNSlots * (n + 1);
+  int* vt_owner = reinterpret_cast<int*>(reinterpret_cast<char*>(scratch) + list_b + off_b + meta_b);
+  void* vt = reinterpret_cast<char*>(scratch) + vt_off;
   variant_index_kernel<<<1, kIdxThreads, 0, s>>>(plans, n, coff, pitch, list, off, meta);
   auto vx = [&](int slot) { return VIdx{list + (size_t)slot * n, off + (size_t)slot * (n + 1), meta + 2 * slot}; };
   if (p->out_dtype == VP_OUT_F32) {
@@ -917,6 +835,9 @@ cudaError_t launch_resize_fast(const vp_params* p, const vp_clip_plan* plans, in
     launch_fast<KV_STRONG, false>(kp, plans, vx(2), frames, coff, pitch, pi, icap, pvv, vcap, s);
     launch_copy<false>(kp, plans, vx(3), frames, coff, pitch, pi, icap, pvv, vcap, s);
   }
+  const cudaError_t re = launch_resize_ring(kp, plans, vx(4), frames, coff, pitch, pi, icap, pvv, vcap, n, vt, vt_owner,
+                                            g_num_sms, s);
+  if (re != cudaSuccess) return re;
   return cudaFreeAsync(scratch, s);
 }
 

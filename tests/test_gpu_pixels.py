@@ -109,6 +109,67 @@ def test_identity_copy_variant(dtype, patch, tp):
     _full_compare(pre, clips)
 
 
+def _aligned_compare(pre, clips, kind="noise"):
+    """As _full_compare, with 16-B aligned row pitches (the TMA variants need them)."""
+    pl = pre.plan(clips)
+    op = oracle_params(pre.params)
+    oplans, _ = O.plan_batch(op, clips)
+    fl = host_frames(oplans, kind)
+    buf, offs, pit = pack_frames(fl, [(3 * c["width"] + 15) // 16 * 16 for c in clips])
+    out = pre.run(pl, buf, offs, pit)
+    torch.cuda.synchronize()
+    ref = O.process_batch(op, clips, [f if f is not None else np.zeros((1, 1, 1, 3), np.uint8) for f in fl],
+                          plans=oplans)
+    assert out["video_grid_thw"].cpu().numpy().tolist() == ref["video_grid_thw"].tolist()
+    assert_pixels(out["pixel_values"].cpu(), ref["pixel_values_images"], "images")
+    assert_pixels(out["pixel_values_videos"].cpu(), ref["pixel_values_videos"], "videos")
+    return pl
+
+
+CLIP_MEAN, CLIP_STD = (0.48145466, 0.4578275, 0.40821073), (0.26862954, 0.26130258, 0.27577711)
+
+
+@pytest.fixture
+def ring_enabled(monkeypatch):
+    """KV_RING is opt-in (VP_RING=1, read by vp_plan_frames on every call)."""
+    monkeypatch.setenv("VP_RING", "1")
+
+
+@pytest.mark.parametrize("dtype", [1, 0])
+@pytest.mark.parametrize("tp", [1, 2, 3])
+def test_ring_variant(dtype, tp, ring_enabled):
+    """KV_RING (one warp per CTA, vertical + horizontal register rings): downscales from ~1.03x to ~3.1x,
+    identity on one axis, several strips with a ragged last strip, 30-row H blocks with a ragged last
+    block, temporal padding (n < tp and n not a multiple of tp), images filling tp slots, CLIP mean/std."""
+    import paper_2604_16893_b200 as vp
+    pre = vp.VisualPreprocessor(max_frames=max(tp, 5), temporal_patch_size=tp, video_max_pixels=32768,
+                                image_max_pixels=65536, out_dtype=dtype, mean=CLIP_MEAN, std=CLIP_STD)
+    clips = [I.clip(9, 2.0, 250, 500),        # 1.95x both axes -> 128 x 256: 6 strips (last 16 wide)
+             I.image(64, 330),                # identity rows, 1.03x columns
+             I.image(330, 64),                # 1.03x rows, identity columns (one strip)
+             I.clip(3, 1.0, 390, 700),        # ~3.1x -> 128 x 224: strips of 32
+             I.clip(1, 1.0, 250, 500),        # n = 1 < tp: padded
+             I.image(250, 500)]
+    pl = _aligned_compare(pre, clips)
+    kv = pl.plans_host["kernel_variant"][:len(clips)].tolist()
+    assert kv.count(5) >= 5, kv
+
+
+@pytest.mark.parametrize("seed", range(3))
+def test_ring_random_downscales(seed, ring_enabled):
+    import paper_2604_16893_b200 as vp
+    rng = random.Random(500 + seed)
+    tp = rng.choice([1, 2])
+    pre = vp.VisualPreprocessor(max_frames=rng.choice([2, 3, 4]), temporal_patch_size=tp,
+                                video_max_pixels=rng.choice([16384, 40000, 90000]), image_max_pixels=65536,
+                                out_dtype=rng.choice([0, 1]))
+    clips = []
+    for _ in range(rng.randint(2, 5)):
+        h, w = rng.randint(40, 700), rng.randint(40, 700)
+        clips.append(I.image(h, w) if rng.random() < 0.3 else I.clip(rng.randint(1, 9), 2.0, h, w))
+    _aligned_compare(pre, clips)
+
+
 def test_cfg2_one_clip_full():
     """BASELINE cfg2 at full size, compared element by element (64 frames 720p -> 384x672)."""
     import paper_2604_16893_b200 as vp
