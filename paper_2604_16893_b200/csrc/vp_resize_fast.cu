@@ -71,18 +71,35 @@ __device__ __forceinline__ void ring_row(Acc& acc, const float (&w)[kRing], cons
   }
 }
 
-// store the finished output row of slot S as 4 pixel-major float4 (RGB + pad) and clear the slot
+// Retired-row layout: footprint pixel x (float4 RGB + pad) sits at float4 index vpos(x), an XOR swizzle of
+// the 16-B granule inside each 128-B group of 8 pixels.  The V lanes' retire stores (pixels 4L + k, lane L)
+// then hit 8 distinct granules per 8 lanes (conflict-free), and the H lanes' tap reads (pixels ~2*scale
+// apart) spread over the granules instead of piling onto two or three of them.
+__device__ __forceinline__ int vpos(int x) { return (x & ~7) | ((x ^ (x >> 3)) & 7); }
+
+// store the finished output row of slot S as 4 pixel-major float4 (RGB + pad) at the row's swizzled
+// positions off[k] of this lane's pixels, and clear the slot
 template <int S>
-__device__ __forceinline__ void retire_slot(Acc& acc, float4* __restrict__ dst, bool active) {
+__device__ __forceinline__ void retire_slot(Acc& acc, float4* __restrict__ row, const int (&off)[4], bool active) {
   if (active) {
     const float2* a = acc[S];
-    dst[0] = make_float4(a[0].x, a[0].y, a[1].x, 0.f);
-    dst[1] = make_float4(a[1].y, a[2].x, a[2].y, 0.f);
-    dst[2] = make_float4(a[3].x, a[3].y, a[4].x, 0.f);
-    dst[3] = make_float4(a[4].y, a[5].x, a[5].y, 0.f);
+    row[off[0]] = make_float4(a[0].x, a[0].y, a[1].x, 0.f);
+    row[off[1]] = make_float4(a[1].y, a[2].x, a[2].y, 0.f);
+    row[off[2]] = make_float4(a[3].x, a[3].y, a[4].x, 0.f);
+    row[off[3]] = make_float4(a[4].y, a[5].x, a[5].y, 0.f);
   }
 #pragma unroll
   for (int q = 0; q < 6; ++q) acc[S][q] = make_float2(0.f, 0.f);
+}
+
+// 4 bytes of w -> two float2 pairs (b0,b1), (b2,b3): PRMT builds the float 2^23 + b (exact), FADD2 removes
+// 2^23.  ALU + FMA pipes instead of I2F.U8 (16/clk/SM on B200, measured: scripts/ubench.cu).
+__device__ __forceinline__ void bytes_to_f2(uint32_t w, float2& lo, float2& hi) {
+  const float2 mm = make_float2(-8388608.f, -8388608.f);
+  lo = __fadd2_rn(make_float2(__uint_as_float(__byte_perm(w, 0x4B000000u, 0x7540u)),
+                              __uint_as_float(__byte_perm(w, 0x4B000000u, 0x7541u))), mm);
+  hi = __fadd2_rn(make_float2(__uint_as_float(__byte_perm(w, 0x4B000000u, 0x7542u)),
+                              __uint_as_float(__byte_perm(w, 0x4B000000u, 0x7543u))), mm);
 }
 
 template <bool kF32>
@@ -291,7 +308,7 @@ resize_fast_kernel(FKParams kp, const vp_clip_plan* __restrict__ plans, const VI
         const Strip st = strip_of(pl, ws, (int)(local % nstrips));
         const int px_lane = warp * kWarpPx + lane * 4;      // this lane's first pixel (relative to pa)
         const bool vactive = px_lane < st.np;
-        float4* vdst_base = vbuf + px_lane;
+        const int voff[4] = {vpos(px_lane), vpos(px_lane + 1), vpos(px_lane + 2), vpos(px_lane + 3)};
         Acc acc;
 #pragma unroll
         for (int r = 0; r < kRing; ++r)
@@ -329,19 +346,16 @@ resize_fast_kernel(FKParams kp, const vp_clip_plan* __restrict__ plans, const VI
                 __syncwarp();                                                                   \
                 if (lane == 0) issue_group(used / kGrp); \
               }                                                                                 \
-              float2 fv[6];                                                                     \
-              fv[0] = make_float2((float)(r0 & 0xffu), (float)((r0 >> 8) & 0xffu));            \
-              fv[1] = make_float2((float)((r0 >> 16) & 0xffu), (float)(r0 >> 24));             \
-              fv[2] = make_float2((float)(r1 & 0xffu), (float)((r1 >> 8) & 0xffu));            \
-              fv[3] = make_float2((float)((r1 >> 16) & 0xffu), (float)(r1 >> 24));             \
-              fv[4] = make_float2((float)(r2 & 0xffu), (float)((r2 >> 8) & 0xffu));            \
-              fv[5] = make_float2((float)((r2 >> 16) & 0xffu), (float)(r2 >> 24));             \
+              float2 fv[6];                   /* bytes (2q, 2q+1) as exact floats (PRMT + FADD2) */ \
+              bytes_to_f2(r0, fv[0], fv[1]);                                                    \
+              bytes_to_f2(r1, fv[2], fv[3]);                                                    \
+              bytes_to_f2(r2, fv[4], fv[5]);                                                    \
               const float w5[kRing] = {wa.x, wa.y, wa.z, wa.w, wb.x};                           \
               ring_row<U>(acc, w5, fv);                                                         \
             }                                                                                   \
             const uint32_t vs = vrow % kCapR, vp2 = vs >> 1, vph = (vrow / kCapR) & 1;          \
             if ((vrow & 1) == 0) mbar_wait(&vempty[vp2], vph ^ 1);    /* once per row pair */   \
-            retire_slot<U>(acc, vdst_base + vs * kRowPx, vactive);                              \
+            retire_slot<U>(acc, vbuf + vs * kRowPx, voff, vactive);                             \
             __syncwarp();                                                                       \
             if (lane == 0) mbar_arrive(&vfull[vp2]);                                            \
             ++vrow;                                                                             \
@@ -425,6 +439,11 @@ resize_fast_kernel(FKParams kp, const vp_clip_plan* __restrict__ plans, const VI
       const bool hact = ht < npairs;
       const int ja = 2 * ht;
       const int xu = hact ? hx[ht] : 0;
+      // swizzled float4 indices of this lane's taps (kept in registers for the MILD union)
+      constexpr int kOffRegs = UL <= 11 ? UL : 1;
+      int toff[kOffRegs];
+#pragma unroll
+      for (int u = 0; u < kOffRegs; ++u) toff[u] = vpos(xu + u);
       // column part of the output element index (O8): (wb*m^2 + mw)*D + px  (channel part added per c)
       int colpart;
       {
@@ -452,25 +471,21 @@ resize_fast_kernel(FKParams kp, const vp_clip_plan* __restrict__ plans, const VI
         if (writable && hact) {
           const float4* v0 = vbuf + s0 * kRowPx;
           const float4* v1 = vbuf + (two ? s1 : s0) * kRowPx;
-          // accumulators per (column, row): RG as a float2 (FFMA2 on the LDS.128 result's .xy pair, no
-          // repacking) and B as a float
-          float2 rg00 = make_float2(0.f, 0.f), rg01 = rg00, rg10 = rg00, rg11 = rg00;  // [col a/b][row 0/1]
-          float b00 = 0.f, b01 = 0.f, b10 = 0.f, b11 = 0.f;
+          // accumulators per (channel, row) over the column pair (col a, col b): each tap is 3 FFMA2 per row,
+          // the pixel's channel value broadcast against the pair's weights (w_a, w_b)
+          float2 ar0 = make_float2(0.f, 0.f), ag0 = ar0, ab0 = ar0, ar1 = ar0, ag1 = ar0, ab1 = ar0;
           const float2* wr = reinterpret_cast<const float2*>(wh) + ht * UL;
 #pragma unroll
           for (int u = 0; u < UL; ++u) {
             const float2 wp = wr[u];                           // (col a, col b) weights at pixel xu+u
-            const float4 q0 = v0[xu + u], q1 = v1[xu + u];     // rows i, i+1
-            const float2 wwa = make_float2(wp.x, wp.x), wwb = make_float2(wp.y, wp.y);
-            const float2 g0 = make_float2(q0.x, q0.y), g1 = make_float2(q1.x, q1.y);
-            rg00 = __ffma2_rn(wwa, g0, rg00);
-            rg01 = __ffma2_rn(wwa, g1, rg01);
-            rg10 = __ffma2_rn(wwb, g0, rg10);
-            rg11 = __ffma2_rn(wwb, g1, rg11);
-            b00 = fmaf(wp.x, q0.z, b00);
-            b01 = fmaf(wp.x, q1.z, b01);
-            b10 = fmaf(wp.y, q0.z, b10);
-            b11 = fmaf(wp.y, q1.z, b11);
+            const int o = UL <= 11 ? toff[u < kOffRegs ? u : 0] : vpos(xu + u);
+            const float4 q0 = v0[o], q1 = v1[o];               // rows i, i+1
+            ar0 = __ffma2_rn(make_float2(q0.x, q0.x), wp, ar0);
+            ag0 = __ffma2_rn(make_float2(q0.y, q0.y), wp, ag0);
+            ab0 = __ffma2_rn(make_float2(q0.z, q0.z), wp, ab0);
+            ar1 = __ffma2_rn(make_float2(q1.x, q1.x), wp, ar1);
+            ag1 = __ffma2_rn(make_float2(q1.y, q1.y), wp, ag1);
+            ab1 = __ffma2_rn(make_float2(q1.z, q1.z), wp, ab1);
           }
           // normalise (O6) x = v*scale_c + bias_c as FFMA2 over the column pair, then clamp (C12) in the
           // output domain: clamp(v,0,255)*s+b == clamp(v*s+b, b, 255*s+b) (s > 0), and for bf16
@@ -478,12 +493,12 @@ resize_fast_kernel(FKParams kp, const vp_clip_plan* __restrict__ plans, const VI
           const float2 s0 = make_float2(kp.scale[0], kp.scale[0]), o0 = make_float2(kp.bias[0], kp.bias[0]);
           const float2 s1 = make_float2(kp.scale[1], kp.scale[1]), o1 = make_float2(kp.bias[1], kp.bias[1]);
           const float2 s2 = make_float2(kp.scale[2], kp.scale[2]), o2 = make_float2(kp.bias[2], kp.bias[2]);
-          const float2 nr0 = __ffma2_rn(make_float2(rg00.x, rg10.x), s0, o0);
-          const float2 ng0 = __ffma2_rn(make_float2(rg00.y, rg10.y), s1, o1);
-          const float2 nb0 = __ffma2_rn(make_float2(b00, b10), s2, o2);
-          const float2 nr1 = __ffma2_rn(make_float2(rg01.x, rg11.x), s0, o0);
-          const float2 ng1 = __ffma2_rn(make_float2(rg01.y, rg11.y), s1, o1);
-          const float2 nb1 = __ffma2_rn(make_float2(b01, b11), s2, o2);
+          const float2 nr0 = __ffma2_rn(ar0, s0, o0);
+          const float2 ng0 = __ffma2_rn(ag0, s1, o1);
+          const float2 nb0 = __ffma2_rn(ab0, s2, o2);
+          const float2 nr1 = __ffma2_rn(ar1, s0, o0);
+          const float2 ng1 = __ffma2_rn(ag1, s1, o1);
+          const float2 nb1 = __ffma2_rn(ab1, s2, o2);
           auto clampf2 = [&](float2 v, int c) {
             return make_float2(fminf(fmaxf(v.x, kp.lo[c]), kp.hi[c]), fminf(fmaxf(v.y, kp.lo[c]), kp.hi[c]));
           };
