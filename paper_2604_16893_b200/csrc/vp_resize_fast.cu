@@ -33,8 +33,8 @@ constexpr int kGrp = 4;                   // rows per TMA group (one mbarrier ph
 constexpr int kNGrp = kDepth / kGrp;
 constexpr int kWarpPx = 128;              // pixels per V warp slice (32 lanes x 4 px)
 constexpr int kWarpB = 3 * kWarpPx;       // 384 bytes
-constexpr int kCapR = 4;                  // retired-row buffer rows (V -> H)
-constexpr int kRowPx = kFastPx + 48;      // float4 pixels per buffered row (+ tap slack)
+constexpr int kCapR = 6;                  // retired-row buffer rows (V -> H): 3 row pairs
+constexpr int kRowPx = kFastPx;           // float4 pixels per buffered row (union-slack taps wrap, weight 0)
 
 
 // Footprint of a strip: first pixel (16-aligned so that the byte offset 3*pa is 16-B aligned for TMA)
@@ -75,7 +75,10 @@ __device__ __forceinline__ void ring_row(Acc& acc, const float (&w)[kRing], cons
 // the 16-B granule inside each 128-B group of 8 pixels.  The V lanes' retire stores (pixels 4L + k, lane L)
 // then hit 8 distinct granules per 8 lanes (conflict-free), and the H lanes' tap reads (pixels ~2*scale
 // apart) spread over the granules instead of piling onto two or three of them.
-__device__ __forceinline__ int vpos(int x) { return (x & ~7) | ((x ^ (x >> 3)) & 7); }
+__device__ __forceinline__ int vpos(int x) {
+  x &= kRowPx - 1;                  // union-slack taps past the footprint (zero weight) wrap to finite data
+  return (x & ~7) | ((x ^ (x >> 3)) & 7);
+}
 
 // store the finished output row of slot S as 4 pixel-major float4 (RGB + pad) at the row's swizzled
 // positions off[k] of this lane's pixels, and clear the slot
@@ -121,8 +124,8 @@ struct FastCfg {
   static constexpr int MAXWS = kFastMaxWs;
   static constexpr size_t OFF_STG = 0;                                                   // V staging
   static constexpr size_t OFF_VBUF = OFF_STG + (size_t)kNVW * kDepth * kWarpB;          // retired rows
-  static constexpr size_t OFF_WROW = OFF_VBUF + (size_t)kCapR * kRowPx * 16;
-  static constexpr size_t OFF_Y1 = OFF_WROW + (size_t)kInHMax * 32;
+  static constexpr size_t OFF_WROW = OFF_VBUF + (size_t)kCapR * kRowPx * 16;   // float4 [kInHMax] + float [kInHMax]
+  static constexpr size_t OFF_Y1 = OFF_WROW + (size_t)kInHMax * 20;
   static constexpr size_t OFF_WH = OFF_Y1 + (size_t)kOutHMax * 4;
   static constexpr size_t OFF_HX = OFF_WH + (size_t)kWhFloats * 4;
   static constexpr size_t OFF_BAR = (OFF_HX + (size_t)MAXWS * 4 + 15) & ~(size_t)15;
@@ -141,7 +144,7 @@ struct ProdItem {
 };
 
 template <int VARIANT>
-__device__ __noinline__ ProdItem producer_open(const vp_clip_plan* __restrict__ plans, const VIdx vx, int cnt, int w,
+__device__ __forceinline__ ProdItem producer_open(const vp_clip_plan* __restrict__ plans, const VIdx vx, int cnt, int w,
                                                const uint8_t* __restrict__ frames,
                                                const int64_t* __restrict__ clip_off,
                                                const int64_t* __restrict__ pitch_arr, int64_t item, int64_t my_b) {
@@ -185,7 +188,9 @@ resize_fast_kernel(FKParams kp, const vp_clip_plan* __restrict__ plans, const VI
   extern __shared__ __align__(128) unsigned char smem[];
   uint8_t* stage_all = smem + Cfg::OFF_STG;
   float4* vbuf = reinterpret_cast<float4*>(smem + Cfg::OFF_VBUF);
-  float* wrow = reinterpret_cast<float*>(smem + Cfg::OFF_WROW);     // [kInHMax][8] vertical weights
+  // vertical weights per source row: w[0..3] (float4) and w[4] of its live output rows i0..i0+4
+  float4* w4t = reinterpret_cast<float4*>(smem + Cfg::OFF_WROW);
+  float* w1t = reinterpret_cast<float*>(smem + Cfg::OFF_WROW + (size_t)kInHMax * 16);
   int* y1t = reinterpret_cast<int*>(smem + Cfg::OFF_Y1);
   float* wh = reinterpret_cast<float*>(smem + Cfg::OFF_WH);
   int* hx = reinterpret_cast<int*>(smem + Cfg::OFF_HX);
@@ -225,35 +230,45 @@ resize_fast_kernel(FKParams kp, const vp_clip_plan* __restrict__ plans, const VI
     uint32_t rslot = 0, rphase = 0;   // staging ring position of the next row to read
     uint32_t vrow = 0;                // running count of retired rows (vbuf slot = vrow % kCapR)
     int cached_clip = -1;
-    // producer state (meaningful in lane 0 only): current slice source row pointer + rows left
+    // TMA producer: warp-uniform state (every lane tracks it), copies / barrier ops predicated to lane 0,
+    // so the refill is not a divergent branch.  A group of kGrp rows inside one item is one expect_tx.
+    const bool l0 = lane == 0;
     ProdItem pit = {nullptr, 0, my_a, 0, 0};
+    int64_t pnext = my_a;             // next item to open
     const uint8_t* psrc = nullptr;
     int prows = 0;
-    auto issue = [&](uint32_t slot) {             // one row into staging slot `slot` (group barrier slot/4)
-      if (prows == 0) {
-        if (pit.src != nullptr || pit.item == my_a) {
-          pit = producer_open<VARIANT>(plans, vx, cnt, warp, frames, clip_off, pitch_arr,
-                                       pit.src != nullptr ? pit.item + 1 : my_a, my_b);
-          if (pit.src == nullptr) pit.item = -1;       // exhausted
-          psrc = pit.src;
-          prows = pit.in_h;
-        }
-        if (prows == 0) return;
-      }
-      if (pit.nbytes > 0) {
-        mbar_expect_tx(&full[slot / kGrp], (uint32_t)pit.nbytes);
-        tma_bulk_g2s(stage + (size_t)slot * kWarpB, psrc, (uint32_t)pit.nbytes, &full[slot / kGrp]);
-      }
-      psrc += pit.pitch;
-      --prows;
-    };
     auto issue_group = [&](uint32_t g) {          // refill the kGrp slots of group g, then arrive once
+      // opaque copy of g (nvcc 12.9 CSE workaround, see vp_resize_ring.cu)
+      asm volatile("mov.b32 %0, %0;" : "+r"(g));
+      if (prows >= kGrp) {
+        mbar_expect_tx_if(&full[g], (uint32_t)(kGrp * pit.nbytes), l0);
 #pragma unroll
-      for (int q = 0; q < kGrp; ++q) issue(g * kGrp + q);
-      mbar_arrive(&full[g]);
+        for (int q = 0; q < kGrp; ++q)
+          tma_bulk_g2s_if(stage + (size_t)(g * kGrp + q) * kWarpB, psrc + (int64_t)q * pit.pitch,
+                          (uint32_t)pit.nbytes, &full[g], l0 && pit.nbytes > 0);
+        psrc += (int64_t)kGrp * pit.pitch;
+        prows -= kGrp;
+      } else {
+#pragma unroll 1
+        for (int q = 0; q < kGrp; ++q) {
+          if (prows == 0 && pnext < my_b) {
+            pit = producer_open<VARIANT>(plans, vx, cnt, warp, frames, clip_off, pitch_arr, pnext, my_b);
+            ++pnext;
+            psrc = pit.src;
+            prows = pit.in_h;
+          }
+          if (prows > 0) {
+            mbar_expect_tx_if(&full[g], (uint32_t)pit.nbytes, l0);
+            tma_bulk_g2s_if(stage + (size_t)(g * kGrp + q) * kWarpB, psrc, (uint32_t)pit.nbytes, &full[g],
+                            l0 && pit.nbytes > 0);
+            psrc += pit.pitch;
+            --prows;
+          }
+        }
+      }
+      mbar_arrive_if(&full[g], l0);
     };
-    if (lane == 0)
-      for (uint32_t g = 0; g < kNGrp; ++g) issue_group(g);     // prefill
+    for (uint32_t g = 0; g < kNGrp; ++g) issue_group(g);     // prefill
     int64_t item = my_a;
     while (item < my_b) {
       const int j = vfind(vx, cnt, item);
@@ -264,43 +279,31 @@ resize_fast_kernel(FKParams kp, const vp_clip_plan* __restrict__ plans, const VI
       const int nstrips = (pl.out_w + ws - 1) / ws;
       const int in_h = pl.in_h, out_h = pl.out_h;
       if (k != cached_clip) {
-        // ---- vertical tables for this clip (K2), V warps only ----
-        // 1/sum of output row i lives in the unused slots 6,7 of the 8-float row vectors (the ring reads 0..4)
-#define VP_INVS(i) wrow[8 * ((i) >> 1) + 6 + ((i) & 1)]
+        // ---- vertical tables for this clip (K2), V warps only: y1 per output row; per source row y the
+        //      weights of its live rows i0..i0+4 (relative order; 0 where not live), f64 Keys / window sum ----
         named_sync(1, kNVW * 32);
-        for (int i = tid; i < out_h; i += kNVW * 32) {
-          const Win w = window_of(in_h, out_h, i);
-          y1t[i] = w.x1;
-          double s = 0.0;
-          for (int y = w.x0; y < w.x1; ++y) s += keys_d(((double)y - w.c + 0.5) * w.inv);
-          VP_INVS(i) = (float)(s != 0.0 ? 1.0 / s : 1.0);
-        }
+        for (int i = tid; i < out_h; i += kNVW * 32) y1t[i] = window_of(in_h, out_h, i).x1;
         named_sync(1, kNVW * 32);
         const double sc = (double)in_h / (double)out_h;
         const double sup = 2.0 * (sc > 1.0 ? sc : 1.0);
-        // per source row y: weights of its live rows i0..i0+cnt-1 as an aligned 8-float vector
-        // (w[0..cnt) , w[7] = cnt); i0 is implied by the output-row-ordered walk
         for (int y = tid; y < in_h; y += kNVW * 32) {
           int i = (int)floor(((double)y - sup - 0.5) / sc - 0.5);
           if (i < 0) i = 0;
           if (i > out_h) i = out_h;
           while (i > 0 && y1t[i - 1] > y) --i;
           while (i < out_h && y1t[i] <= y) ++i;
-          float wv[8] = {0.f, 0.f, 0.f, 0.f, 0.f, 0.f, 0.f, 0.f};
-          int cnt = 0;
+          float wv[kRing] = {0.f, 0.f, 0.f, 0.f, 0.f};
           for (int r = 0; r < kRing && i + r < out_h; ++r) {
             const Win w = window_of(in_h, out_h, i + r);
             if (w.x0 > y) break;
-            wv[r] = (float)keys_d(((double)y - w.c + 0.5) * w.inv) * VP_INVS(i + r);
-            ++cnt;
+            double s = 0.0;
+            for (int yy = w.x0; yy < w.x1; ++yy) s += keys_d(((double)yy - w.c + 0.5) * w.inv);
+            wv[r] = (float)(keys_d(((double)y - w.c + 0.5) * w.inv) / (s != 0.0 ? s : 1.0));
           }
-          (void)cnt;
-          float4* dst = reinterpret_cast<float4*>(wrow + 8 * y);
-          dst[0] = make_float4(wv[0], wv[1], wv[2], wv[3]);
-          wrow[8 * y + 4] = wv[4];                       // slots 5..7: row-window scratch (VP_INVS)
+          w4t[y] = make_float4(wv[0], wv[1], wv[2], wv[3]);
+          w1t[y] = wv[4];
         }
         named_sync(1, kNVW * 32);
-#undef VP_INVS
         cached_clip = k;
       }
       for (; item < cend && item < my_b; ++item) {
@@ -315,17 +318,22 @@ resize_fast_kernel(FKParams kp, const vp_clip_plan* __restrict__ plans, const VI
 #pragma unroll
           for (int q = 0; q < 6; ++q) acc[r][q] = make_float2(0.f, 0.f);
         int y = 0;
-        // software pipeline: the staged bytes and the weight vector of row y are loaded one row ahead
+        // software pipeline without register copies: row y's staged bytes (n0..n2) are converted first, then
+        // row y+1's bytes are loaded into the same registers; row y's weights (nwa, nwb) feed the FMAs, then
+        // row y+1's weights are loaded over them.
         uint32_t n0 = 0, n1 = 0, n2 = 0;
-        float4 nwa = make_float4(0.f, 0.f, 0.f, 0.f), nwb = nwa;
-        auto load_row = [&](int yy) {
+        float4 nwa = make_float4(0.f, 0.f, 0.f, 0.f);
+        float nwb = 0.f;
+        auto load_bytes = [&]() {
           if ((rslot & (kGrp - 1)) == 0) mbar_wait(&full[rslot / kGrp], rphase);   // once per group
           const uint32_t* sp = reinterpret_cast<const uint32_t*>(stage + rslot * kWarpB) + lane * 3;
           n0 = sp[0]; n1 = sp[1]; n2 = sp[2];
-          const float4* wp = reinterpret_cast<const float4*>(wrow + 8 * yy);
-          nwa = wp[0]; nwb = wp[1];
         };
-        if (in_h > 0) load_row(0);
+        if (in_h > 0) {
+          load_bytes();
+          nwa = w4t[0];
+          nwb = w1t[0];
+        }
         // Output row i lives in ring slot i % kRing.  Unrolling the output-row loop by kRing makes every
         // slot index static: for row i = ib + U, consume the source rows up to its window end y1_i (the
         // first live row of each of them is i), then retire slot U.
@@ -337,21 +345,20 @@ resize_fast_kernel(FKParams kp, const vp_clip_plan* __restrict__ plans, const VI
           if (ib + U < out_h) {                                                                 \
             const int yend = yends[U];                                                          \
             for (; y < yend; ++y) {                                                             \
-              const uint32_t r0 = n0, r1 = n1, r2 = n2;                                         \
-              const float4 wa = nwa, wb = nwb;                                                  \
+              float2 fv[6];                   /* bytes (2q, 2q+1) as exact floats (PRMT + FADD2) */ \
+              bytes_to_f2(n0, fv[0], fv[1]);                                                    \
+              bytes_to_f2(n1, fv[2], fv[3]);                                                    \
+              bytes_to_f2(n2, fv[4], fv[5]);                                                    \
               const uint32_t used = rslot;                                                      \
               if (++rslot == kDepth) { rslot = 0; rphase ^= 1; }                                \
-              if (y + 1 < in_h) load_row(y + 1);                                                \
-              if ((used & 3) == 3) {                                                            \
+              if ((used & 3) == 3) {          /* group fully read: refill it */                 \
                 __syncwarp();                                                                   \
-                if (lane == 0) issue_group(used / kGrp); \
+                issue_group(used / kGrp);                                                       \
               }                                                                                 \
-              float2 fv[6];                   /* bytes (2q, 2q+1) as exact floats (PRMT + FADD2) */ \
-              bytes_to_f2(r0, fv[0], fv[1]);                                                    \
-              bytes_to_f2(r1, fv[2], fv[3]);                                                    \
-              bytes_to_f2(r2, fv[4], fv[5]);                                                    \
-              const float w5[kRing] = {wa.x, wa.y, wa.z, wa.w, wb.x};                           \
+              if (y + 1 < in_h) load_bytes();                                                   \
+              const float w5[kRing] = {nwa.x, nwa.y, nwa.z, nwa.w, nwb};                        \
               ring_row<U>(acc, w5, fv);                                                         \
+              if (y + 1 < in_h) { nwa = w4t[y + 1]; nwb = w1t[y + 1]; }                         \
             }                                                                                   \
             const uint32_t vs = vrow % kCapR, vp2 = vs >> 1, vph = (vrow / kCapR) & 1;          \
             if ((vrow & 1) == 0) mbar_wait(&vempty[vp2], vph ^ 1);    /* once per row pair */   \
@@ -375,7 +382,7 @@ resize_fast_kernel(FKParams kp, const vp_clip_plan* __restrict__ plans, const VI
           if (++rslot == kDepth) { rslot = 0; rphase ^= 1; }
           if ((used & 3) == 3) {
             __syncwarp();
-            if (lane == 0) issue_group(used / kGrp);
+            issue_group(used / kGrp);
           }
           ++y;
         }
@@ -387,7 +394,7 @@ resize_fast_kernel(FKParams kp, const vp_clip_plan* __restrict__ plans, const VI
           if (++rslot == kDepth) { rslot = 0; rphase ^= 1; }
           if ((used & 3) == 3) {
             __syncwarp();
-            if (lane == 0) issue_group(used / kGrp);
+            issue_group(used / kGrp);
           }
         }
       }
