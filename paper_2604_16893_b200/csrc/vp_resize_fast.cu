@@ -318,22 +318,15 @@ resize_fast_kernel(FKParams kp, const vp_clip_plan* __restrict__ plans, const VI
 #pragma unroll
           for (int q = 0; q < 6; ++q) acc[r][q] = make_float2(0.f, 0.f);
         int y = 0;
-        // software pipeline without register copies: row y's staged bytes (n0..n2) are converted first, then
-        // row y+1's bytes are loaded into the same registers; row y's weights (nwa, nwb) feed the FMAs, then
-        // row y+1's weights are loaded over them.
+        // No software prefetch: with 16 warps per SM the LDS latency of a row is covered by other warps, and
+        // loading at the top of the row keeps the loop free of register rotation copies (measured faster).
         uint32_t n0 = 0, n1 = 0, n2 = 0;
-        float4 nwa = make_float4(0.f, 0.f, 0.f, 0.f);
-        float nwb = 0.f;
         auto load_bytes = [&]() {
           if ((rslot & (kGrp - 1)) == 0) mbar_wait(&full[rslot / kGrp], rphase);   // once per group
           const uint32_t* sp = reinterpret_cast<const uint32_t*>(stage + rslot * kWarpB) + lane * 3;
           n0 = sp[0]; n1 = sp[1]; n2 = sp[2];
         };
-        if (in_h > 0) {
-          load_bytes();
-          nwa = w4t[0];
-          nwb = w1t[0];
-        }
+
         // Output row i lives in ring slot i % kRing.  Unrolling the output-row loop by kRing makes every
         // slot index static: for row i = ib + U, consume the source rows up to its window end y1_i (the
         // first live row of each of them is i), then retire slot U.
@@ -345,6 +338,9 @@ resize_fast_kernel(FKParams kp, const vp_clip_plan* __restrict__ plans, const VI
           if (ib + U < out_h) {                                                                 \
             const int yend = yends[U];                                                          \
             for (; y < yend; ++y) {                                                             \
+              load_bytes();                                                                     \
+              const float4 wa = w4t[y];                                                         \
+              const float wb = w1t[y];                                                          \
               float2 fv[6];                   /* bytes (2q, 2q+1) as exact floats (PRMT + FADD2) */ \
               bytes_to_f2(n0, fv[0], fv[1]);                                                    \
               bytes_to_f2(n1, fv[2], fv[3]);                                                    \
@@ -355,10 +351,8 @@ resize_fast_kernel(FKParams kp, const vp_clip_plan* __restrict__ plans, const VI
                 __syncwarp();                                                                   \
                 issue_group(used / kGrp);                                                       \
               }                                                                                 \
-              if (y + 1 < in_h) load_bytes();                                                   \
-              const float w5[kRing] = {nwa.x, nwa.y, nwa.z, nwa.w, nwb};                        \
+              const float w5[kRing] = {wa.x, wa.y, wa.z, wa.w, wb};                             \
               ring_row<U>(acc, w5, fv);                                                         \
-              if (y + 1 < in_h) { nwa = w4t[y + 1]; nwb = w1t[y + 1]; }                         \
             }                                                                                   \
             const uint32_t vs = vrow % kCapR, vp2 = vs >> 1, vph = (vrow / kCapR) & 1;          \
             if ((vrow & 1) == 0) mbar_wait(&vempty[vp2], vph ^ 1);    /* once per row pair */   \
@@ -375,16 +369,6 @@ resize_fast_kernel(FKParams kp, const vp_clip_plan* __restrict__ plans, const VI
           __syncwarp();
           if (lane == 0) mbar_arrive(&vfull[(vrow % kCapR) >> 1]);
           ++vrow;
-        }
-        // the row prefetched beyond the last window (if any) and all rows below it keep the ring in step
-        if (y < in_h) {
-          const uint32_t used = rslot;
-          if (++rslot == kDepth) { rslot = 0; rphase ^= 1; }
-          if ((used & 3) == 3) {
-            __syncwarp();
-            issue_group(used / kGrp);
-          }
-          ++y;
         }
         // source rows below the last window (none for the supported ratios) keep the ring in step
         for (; y < in_h; ++y) {
