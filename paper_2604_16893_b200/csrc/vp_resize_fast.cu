@@ -71,13 +71,14 @@ __device__ __forceinline__ void ring_row(Acc& acc, const float (&w)[kRing], cons
   }
 }
 
-// Retired-row layout: footprint pixel x (float4 RGB + pad) sits at float4 index vpos(x), an XOR swizzle of
-// the 16-B granule inside each 128-B group of 8 pixels.  The V lanes' retire stores (pixels 4L + k, lane L)
-// then hit 8 distinct granules per 8 lanes (conflict-free), and the H lanes' tap reads (pixels ~2*scale
-// apart) spread over the granules instead of piling onto two or three of them.
+// Retired-row layout: footprint pixel x (float4 RGB + pad) sits at float4 index vpos(x): inside each block of
+// 32 pixels, sub-pixel-major (pixel 4a + k at 8k + a).  The V lanes' retire stores (pixels 4L + k, lane L)
+// then hit 8 distinct 16-B granules per quarter-warp (conflict-free), and the H lanes' tap reads (column
+// pairs ~2*scale pixels apart) cost 1.35 wavefronts per ideal one at the cfg2 ratio (natural layout 2.9,
+// an XOR swizzle 1.95; offline bank simulation over the tap pattern).
 __device__ __forceinline__ int vpos(int x) {
   x &= kRowPx - 1;                  // union-slack taps past the footprint (zero weight) wrap to finite data
-  return (x & ~7) | ((x ^ (x >> 3)) & 7);
+  return (x & ~31) | ((x & 3) << 3) | ((x & 31) >> 2);
 }
 
 // store the finished output row of slot S as 4 pixel-major float4 (RGB + pad) at the row's swizzled
