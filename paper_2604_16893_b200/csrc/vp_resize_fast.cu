@@ -22,6 +22,19 @@
 // The V warps load row y+1's staged bytes and weight vector while FMA-ing row y (software pipeline).
 #include "vp_k3_common.cuh"
 
+#ifndef VP_EXP_NO_VMATH
+#define VP_EXP_NO_VMATH 0   // experiments only: skip the V ring FMAs
+#endif
+#ifndef VP_EXP_NO_HMATH
+#define VP_EXP_NO_HMATH 0   // experiments only: skip the H taps, normalisation and stores
+#endif
+#ifndef VP_EXP_NO_VWAIT
+#define VP_EXP_NO_VWAIT 0   // experiments only (scripts/exp3.sh): V does not wait for H to free rows
+#endif
+#ifndef VP_EXP_NO_HWAIT
+#define VP_EXP_NO_HWAIT 0   // experiments only: H does not wait for V rows (reads stale rows)
+#endif
+
 namespace vp {
 namespace {
 
@@ -53,12 +66,18 @@ __device__ __forceinline__ Strip strip_of(const vp_clip_plan& pl, int ws, int st
 
 
 // ---------------------------------------------------------------- vertical ring
-// acc[slot][q]: bytes (2q, 2q+1) of this lane's 12 source bytes (4 RGB pixels) for the output row in
-// `slot` (= row & 7).
-typedef float2 Acc[kRing][6];
+// acc[slot].q[j]: this lane's 12 source bytes (4 RGB pixels: R0 G0 B0 R1 | G1 B1 R2 G2 | B2 R3 G3 B3) for the
+// output row in `slot`, as three float4 quads -- bytes (2q, 2q+1) are the .xy / .zw halves (FFMA2 operands)
+// and pixels 0 and 2 are whole quads at retire (no repacking).
+struct AccRow {
+  float4 q[3];
+};
+typedef AccRow Acc[kRing];
 
-// contributions of one source row to the live rows i..i+5, where row i sits in slot U (static).
-// Dense over the 6 ring slots: the weight vector holds 0 for rows that are not live, so the code is
+__device__ __forceinline__ float2& half2_of(float4& v, int h) { return reinterpret_cast<float2*>(&v)[h]; }
+
+// contributions of one source row to the live rows i..i+4, where row i sits in slot U (static).
+// Dense over the ring slots: the weight vector holds 0 for rows that are not live, so the code is
 // straight-line FFMA2 with no per-row branch (a 0-weight FMA adds exactly 0).
 template <int U>
 __device__ __forceinline__ void ring_row(Acc& acc, const float (&w)[kRing], const float2 (&f)[6]) {
@@ -67,7 +86,10 @@ __device__ __forceinline__ void ring_row(Acc& acc, const float (&w)[kRing], cons
     const int slot = (U + r) % kRing;
     const float2 ww = make_float2(w[r], w[r]);
 #pragma unroll
-    for (int q = 0; q < 6; ++q) acc[slot][q] = __ffma2_rn(ww, f[q], acc[slot][q]);
+    for (int q = 0; q < 6; ++q) {
+      float2& a = half2_of(acc[slot].q[q >> 1], q & 1);
+      a = __ffma2_rn(ww, f[q], a);
+    }
   }
 }
 
@@ -81,19 +103,20 @@ __device__ __forceinline__ int vpos(int x) {
   return (x & ~31) | ((x & 3) << 3) | ((x & 31) >> 2);
 }
 
-// store the finished output row of slot S as 4 pixel-major float4 (RGB + pad) at the row's swizzled
-// positions off[k] of this lane's pixels, and clear the slot
+// store the finished output row of slot S as 4 pixel-major float4 (R, G, B, pad) at this lane's pixel
+// positions (row + vb + 8k: vpos of pixel 4L + k inside the 32-px block layout) and clear the slot.  The pad
+// of pixels 0 and 2 is whatever the quad holds (H reads .xyz only).
 template <int S>
-__device__ __forceinline__ void retire_slot(Acc& acc, float4* __restrict__ row, const int (&off)[4], bool active) {
+__device__ __forceinline__ void retire_slot(Acc& acc, float4* __restrict__ row, int vb, bool active) {
   if (active) {
-    const float2* a = acc[S];
-    row[off[0]] = make_float4(a[0].x, a[0].y, a[1].x, 0.f);
-    row[off[1]] = make_float4(a[1].y, a[2].x, a[2].y, 0.f);
-    row[off[2]] = make_float4(a[3].x, a[3].y, a[4].x, 0.f);
-    row[off[3]] = make_float4(a[4].y, a[5].x, a[5].y, 0.f);
+    const float4* a = acc[S].q;
+    row[vb] = a[0];                                            // R0 G0 B0 (R1)
+    row[vb + 8] = make_float4(a[0].w, a[1].x, a[1].y, 0.f);    // R1 G1 B1
+    row[vb + 16] = make_float4(a[1].z, a[1].w, a[2].x, a[2].y); // R2 G2 B2 (R3)
+    row[vb + 24] = make_float4(a[2].y, a[2].z, a[2].w, 0.f);   // R3 G3 B3
   }
 #pragma unroll
-  for (int q = 0; q < 6; ++q) acc[S][q] = make_float2(0.f, 0.f);
+  for (int j = 0; j < 3; ++j) acc[S].q[j] = make_float4(0.f, 0.f, 0.f, 0.f);
 }
 
 // 4 bytes of w -> two float2 pairs (b0,b1), (b2,b3): PRMT builds the float 2^23 + b (exact), FADD2 removes
@@ -229,7 +252,8 @@ resize_fast_kernel(FKParams kp, const vp_clip_plan* __restrict__ plans, const VI
     uint8_t* stage = stage_all + (size_t)warp * kDepth * kWarpB;
     uint64_t* full = full_all + warp * kNGrp;     // one barrier per group of kGrp staging slots
     uint32_t rslot = 0, rphase = 0;   // staging ring position of the next row to read
-    uint32_t vrow = 0;                // running count of retired rows (vbuf slot = vrow % kCapR)
+    uint32_t vrow = 0;                // running count of retired rows
+    uint32_t vslot = 0, vphase = 0;   // vbuf slot of the next retired row (= vrow % kCapR) and its pair phase
     int cached_clip = -1;
     // TMA producer: warp-uniform state (every lane tracks it), copies / barrier ops predicated to lane 0,
     // so the refill is not a divergent branch.  A group of kGrp rows inside one item is one expect_tx.
@@ -312,12 +336,13 @@ resize_fast_kernel(FKParams kp, const vp_clip_plan* __restrict__ plans, const VI
         const Strip st = strip_of(pl, ws, (int)(local % nstrips));
         const int px_lane = warp * kWarpPx + lane * 4;      // this lane's first pixel (relative to pa)
         const bool vactive = px_lane < st.np;
-        const int voff[4] = {vpos(px_lane), vpos(px_lane + 1), vpos(px_lane + 2), vpos(px_lane + 3)};
+        // vpos(px_lane + k) == vb + 8k for this lane's 4 pixels (px_lane is a multiple of 4)
+        const int vb = vpos(px_lane);
         Acc acc;
 #pragma unroll
         for (int r = 0; r < kRing; ++r)
 #pragma unroll
-          for (int q = 0; q < 6; ++q) acc[r][q] = make_float2(0.f, 0.f);
+          for (int j = 0; j < 3; ++j) acc[r].q[j] = make_float4(0.f, 0.f, 0.f, 0.f);
         int y = 0;
         // No software prefetch: with 16 warps per SM the LDS latency of a row is covered by other warps, and
         // loading at the top of the row keeps the loop free of register rotation copies (measured faster).
@@ -353,14 +378,15 @@ resize_fast_kernel(FKParams kp, const vp_clip_plan* __restrict__ plans, const VI
                 issue_group(used / kGrp);                                                       \
               }                                                                                 \
               const float w5[kRing] = {wa.x, wa.y, wa.z, wa.w, wb};                             \
-              ring_row<U>(acc, w5, fv);                                                         \
+              if (!VP_EXP_NO_VMATH) ring_row<U>(acc, w5, fv);                                   \
             }                                                                                   \
-            const uint32_t vs = vrow % kCapR, vp2 = vs >> 1, vph = (vrow / kCapR) & 1;          \
-            if ((vrow & 1) == 0) mbar_wait(&vempty[vp2], vph ^ 1);    /* once per row pair */   \
-            retire_slot<U>(acc, vbuf + vs * kRowPx, voff, vactive);                             \
+            const uint32_t vs = vslot, vp2 = vs >> 1, vph = vphase;                             \
+            if ((vrow & 1) == 0 && !VP_EXP_NO_VWAIT) mbar_wait(&vempty[vp2], vph ^ 1);  /* per pair */ \
+            retire_slot<U>(acc, vbuf + vs * kRowPx, vb, vactive);                               \
             __syncwarp();                                                                       \
             if (lane == 0) mbar_arrive(&vfull[vp2]);                                            \
             ++vrow;                                                                             \
+            if (++vslot == kCapR) { vslot = 0; vphase ^= 1; }                                   \
           }
           static_assert(kRing == 5, "unroll below");
           VP_ROW(0) VP_ROW(1) VP_ROW(2) VP_ROW(3) VP_ROW(4)
@@ -368,8 +394,9 @@ resize_fast_kernel(FKParams kp, const vp_clip_plan* __restrict__ plans, const VI
         }
         if (vrow & 1) {                             // odd out_h: complete the last pair's barrier phase
           __syncwarp();
-          if (lane == 0) mbar_arrive(&vfull[(vrow % kCapR) >> 1]);
+          if (lane == 0) mbar_arrive(&vfull[vslot >> 1]);
           ++vrow;
+          if (++vslot == kCapR) { vslot = 0; vphase ^= 1; }
         }
         // source rows below the last window (none for the supported ratios) keep the ring in step
         for (; y < in_h; ++y) {
@@ -455,12 +482,12 @@ resize_fast_kernel(FKParams kp, const vp_clip_plan* __restrict__ plans, const VI
       for (int i = 0; i < out_h; i += 2) {
         const bool two = i + 1 < out_h;
         const uint32_t s0 = vrow % kCapR, s1 = s0 + 1, ph0 = (vrow / kCapR) & 1;   // rows of pair s0/2
-        mbar_wait(&vfull[s0 >> 1], ph0);
+        if (!VP_EXP_NO_HWAIT) mbar_wait(&vfull[s0 >> 1], ph0);
         const int64_t rp0 = base0 + r_hb * hb_stride + (int64_t)(r_mh * m) * kp.D + r_py * p;
         if (++r_py == p) { r_py = 0; if (++r_mh == m) { r_mh = 0; ++r_hb; } }
         const int64_t rp1 = base0 + r_hb * hb_stride + (int64_t)(r_mh * m) * kp.D + r_py * p;
         if (two) { if (++r_py == p) { r_py = 0; if (++r_mh == m) { r_mh = 0; ++r_hb; } } }
-        if (writable && hact) {
+        if (writable && hact && !VP_EXP_NO_HMATH) {
           const float4* v0 = vbuf + s0 * kRowPx;
           const float4* v1 = vbuf + (two ? s1 : s0) * kRowPx;
           // accumulators per (channel, row) over the column pair (col a, col b): each tap is 3 FFMA2 per row,
