@@ -218,6 +218,56 @@ def test_cfg4_sampled():
     _sampled_compare(vp.VisualPreprocessor(**params), clips, n_samples=3000)
 
 
+def test_cfg5_bench_launch_sampled():
+    """The bench's own workload and launch configuration (bench.py cfg5): 512 full-size cfg2 clips (90.6 GB of
+    device-synthesised noise frames, seed = clip index, as bench.py), bf16 output, one K3 call over the whole
+    batch; 16 (clip, source frame) pairs x 128 sampled outputs are recomputed one by one by the oracle from
+    the host twin of the frame generator."""
+    import paper_2604_16893_b200 as vp
+    params = I.qwen3_params(max_frames=64)
+    clips = [I.clip(1800, 30.0, 720, 1280)] * 512
+    pre = vp.VisualPreprocessor(**params)
+    pl = pre.plan(clips)
+    ph = pl.plans_host
+    off, pitch, total = pre.frames_layout(pl)
+    frames = torch.empty(total, dtype=torch.uint8, device="cuda")
+    idx_host = pl.frame_indices.cpu().numpy()
+    for k in range(len(clips)):
+        n = int(ph["n_frames"][k])
+        ids = torch.from_numpy(idx_host[ph["index_offset"][k]: ph["index_offset"][k] + n].copy()).cuda()
+        vp.synth_frames(vp.VP_SYNTH_NOISE, k, ids, 720, 1280, frames[off[k]:], int(pitch[k]))
+    out = pre.run(pl, frames, torch.from_numpy(off).cuda(), torch.from_numpy(pitch).cuda(), strict=True)
+    torch.cuda.synchronize()
+    del frames
+    op = oracle_params(pre.params)
+    oplans, _ = O.plan_batch(op, clips[:1])
+    o = oplans[0]
+    p, m, tp = op["patch_size"], op["merge_size"], op["temporal_patch_size"]
+    pv = out["pixel_values_videos"]
+    rng = np.random.default_rng(5)
+    rows, ref = [], []
+    per_clip_rows = o.patches
+    for k in rng.choice(len(clips), 16, replace=False):
+        k = int(k)
+        f = int(rng.integers(o.n))                      # a sampled source frame of clip k
+        fid = int(idx_host[ph["index_offset"][k] + f])
+        fr = I.frames_u8("noise", k, [fid], 720, 1280)[0]
+        cache = {}
+        got = 0
+        while got < 128:
+            r, q = int(rng.integers(per_clip_rows)), int(rng.integers(pv.shape[1]))
+            slot, y, x, c = O.patch_coords(r, q, o.grid, p, m, tp)
+            if min(slot, o.n - 1) != f:
+                continue
+            v = O.resize_pixel(fr, o.out_h, o.out_w, y, x, c, cache)
+            ref.append((v / 255.0 - op["mean"][c]) / op["std"][c])
+            rows.append((int(ph["patch_offset"][k]) + r, q))
+            got += 1
+    idx = torch.tensor(rows, dtype=torch.int64, device=pv.device)
+    assert_pixels(pv[idx[:, 0], idx[:, 1]].cpu(), np.array(ref), "cfg5 videos")
+    assert out["video_grid_thw"].cpu().tolist() == [[32, 24, 42]] * 512
+
+
 def test_determinism_three_runs():
     """AC12: three runs are byte-identical."""
     import paper_2604_16893_b200 as vp
