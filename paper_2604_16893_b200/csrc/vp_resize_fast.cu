@@ -22,6 +22,12 @@
 // The V warps load row y+1's staged bytes and weight vector while FMA-ing row y (software pipeline).
 #include "vp_k3_common.cuh"
 
+#ifndef VP_VREGS
+#define VP_VREGS 152        // setmaxnreg split between the V and H warpgroups (sum 256)
+#endif
+#ifndef VP_HREGS
+#define VP_HREGS 104
+#endif
 #ifndef VP_EXP_NO_VMATH
 #define VP_EXP_NO_VMATH 0   // experiments only: skip the V ring FMAs
 #endif
@@ -248,7 +254,7 @@ resize_fast_kernel(FKParams kp, const vp_clip_plan* __restrict__ plans, const VI
 
   if (warp < kNVW) {
     // ============================================================ V warps: vertical ring
-    asm volatile("setmaxnreg.inc.sync.aligned.u32 152;\n" ::: "memory");
+    asm volatile("setmaxnreg.inc.sync.aligned.u32 %0;\n" :: "n"(VP_VREGS) : "memory");
     uint8_t* stage = stage_all + (size_t)warp * kDepth * kWarpB;
     uint64_t* full = full_all + warp * kNGrp;     // one barrier per group of kGrp staging slots
     uint32_t rslot = 0, rphase = 0;   // staging ring position of the next row to read
@@ -415,7 +421,7 @@ resize_fast_kernel(FKParams kp, const vp_clip_plan* __restrict__ plans, const VI
   }
 
   // ============================================================ H warps: horizontal pass + store
-  asm volatile("setmaxnreg.dec.sync.aligned.u32 104;\n" ::: "memory");
+  asm volatile("setmaxnreg.dec.sync.aligned.u32 %0;\n" :: "n"(VP_HREGS) : "memory");
   const int ht = tid - kNVW * 32;       // 0..127
   const int p = kp.p, m = kp.m, tp = kp.tp, B = m * p;
   uint32_t vrow = 0;
