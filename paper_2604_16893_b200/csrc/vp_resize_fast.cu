@@ -22,6 +22,9 @@
 // The V warps load row y+1's staged bytes and weight vector while FMA-ing row y (software pipeline).
 #include "vp_k3_common.cuh"
 
+#ifndef VP_H_SLEEP
+#define VP_H_SLEEP 0        // H warps wait for V rows with a suspend-time hint instead of spinning
+#endif
 #ifndef VP_VREGS
 #define VP_VREGS 152        // setmaxnreg split between the V and H warpgroups (sum 256)
 #endif
@@ -488,7 +491,10 @@ resize_fast_kernel(FKParams kp, const vp_clip_plan* __restrict__ plans, const VI
       for (int i = 0; i < out_h; i += 2) {
         const bool two = i + 1 < out_h;
         const uint32_t s0 = vrow % kCapR, s1 = s0 + 1, ph0 = (vrow / kCapR) & 1;   // rows of pair s0/2
-        if (!VP_EXP_NO_HWAIT) mbar_wait(&vfull[s0 >> 1], ph0);
+        if (!VP_EXP_NO_HWAIT) {
+          if (VP_H_SLEEP) mbar_wait_sleep(&vfull[s0 >> 1], ph0);
+          else mbar_wait(&vfull[s0 >> 1], ph0);
+        }
         const int64_t rp0 = base0 + r_hb * hb_stride + (int64_t)(r_mh * m) * kp.D + r_py * p;
         if (++r_py == p) { r_py = 0; if (++r_mh == m) { r_mh = 0; ++r_hb; } }
         const int64_t rp1 = base0 + r_hb * hb_stride + (int64_t)(r_mh * m) * kp.D + r_py * p;
