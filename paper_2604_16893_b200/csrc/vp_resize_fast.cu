@@ -4,22 +4,25 @@
 // Work item = (clip, source frame f, strip of Ws <= 256 output columns).  A CTA walks the item's
 // source rows top to bottom exactly once with two warp-specialised groups:
 //   * 4 V warps (vertical pass).  Each V warp owns a 128-pixel (384-byte) slice of the strip's
-//     source footprint and is its own TMA producer: lane 0 keeps kDepth rows of its slice in flight
-//     with cp.async.bulk (global -> smem, completion on a per-warp mbarrier); lane L converts its 4
-//     pixels (12 bytes, I2F.U8) once per source row and FMAs them (FFMA2) into the <= 8 output rows
-//     live at that row, held in a register ring acc[5].  Output row i lives in slot i % 5; the
-//     output-row loop is unrolled by 5 so every slot index is static (no dynamic register indexing,
-//     no accumulator shuffles), and each source row dispatches once on its live count.
-//   * 4 H warps (horizontal pass).  Retired rows arrive through a 4-row smem buffer, pixel-major
-//     (float4 = RGB + pad) with mbarrier hand-off; each H thread computes 2 adjacent output columns x
-//     2 rows x 3 channels (LDS.128 + FFMA2, horizontal weights in registers for MILD), clamps,
-//     normalises and stores bf16x2 / float2 straight into the HF patch layout, once per temporal slot
-//     the frame fills (O7) -- every output element is written exactly once.
-// Registers are rebalanced between the warpgroups with setmaxnreg (V holds the 60-register ring).
-// Per-clip tables (cached across a CTA's consecutive items): per source row an aligned 8-float vector
-// of the weights of its live output rows + the live count (fp32 from f64); windows are trimmed of
-// exact-zero taps (identity axes become 1-tap copies).  Per item: the strip's horizontal weights.
-// The V warps load row y+1's staged bytes and weight vector while FMA-ing row y (software pipeline).
+//     source footprint and keeps kDepth rows of it in flight with cp.async.bulk (global -> smem,
+//     completion on per-group mbarriers); the producer state is warp-uniform and only the copy /
+//     barrier instructions are predicated to lane 0.  Lane L converts its 4 pixels (12 bytes) once per
+//     source row (PRMT into 2^23 + b, FADD2 -2^23: exact) and FMAs them (FFMA2, broadcast weight) into
+//     the output rows live at that row, held in a register ring acc[5] of float4 quads.  Output row i
+//     lives in slot i % 5; the output-row loop is unrolled by 5 so every slot index is static (no
+//     dynamic register indexing, no accumulator shuffles).
+//   * 4 H warps (horizontal pass).  Retired rows arrive through a 6-row smem buffer in row pairs
+//     (mbarrier hand-off each way), pixel-major float4 (RGB + pad) in a sub-pixel-major layout inside
+//     32-pixel blocks (vpos: conflict-free V stores, 1.35x H read wavefronts).  Each H thread computes a
+//     column pair x 2 rows x 3 channels over the pair's union window (LDS.128 per tap and row, 3 FFMA2:
+//     the pixel broadcast against the pair's weights), normalises, clamps in the output domain and
+//     stores bf16x2 / float2 straight into the HF patch layout, once per temporal slot the frame fills
+//     (O7) -- every output element is written exactly once.
+// Registers are rebalanced between the warpgroups with setmaxnreg (V 152: the 60-register ring; H 104).
+// Per-clip tables (cached across a CTA's consecutive items): per source row the fp32 weights (f64 Keys /
+// f64 window sum) of its live output rows; windows are trimmed of exact-zero taps (identity axes become
+// 1-tap copies).  Per item: the strip's horizontal weights.  Measurements behind each choice: DESIGN.md
+// section 6 and profiles/r03_summary.md.
 #include "vp_k3_common.cuh"
 
 #ifndef VP_H_SLEEP
