@@ -25,6 +25,9 @@
 // section 6 and profiles/r03_summary.md.
 #include "vp_k3_common.cuh"
 
+#ifndef VP_CVT_I2F
+#define VP_CVT_I2F 2        // how many of the 3 staged words per row convert on XU (I2F) instead of PRMT+FADD2
+#endif
 #ifndef VP_H_SLEEP
 #define VP_H_SLEEP 0        // H warps wait for V rows with a suspend-time hint instead of spinning
 #endif
@@ -133,6 +136,10 @@ __device__ __forceinline__ void retire_slot(Acc& acc, float4* __restrict__ row, 
 
 // 4 bytes of w -> two float2 pairs (b0,b1), (b2,b3): PRMT builds the float 2^23 + b (exact), FADD2 removes
 // 2^23.  ALU + FMA pipes instead of I2F.U8 (16/clk/SM on B200, measured: scripts/ubench.cu).
+__device__ __forceinline__ void bytes_to_f2_i2f(uint32_t w, float2& lo, float2& hi) {   // XU pipe (I2F.U8)
+  lo = make_float2((float)(w & 0xffu), (float)((w >> 8) & 0xffu));
+  hi = make_float2((float)((w >> 16) & 0xffu), (float)(w >> 24));
+}
 __device__ __forceinline__ void bytes_to_f2(uint32_t w, float2& lo, float2& hi) {
   const float2 mm = make_float2(-8388608.f, -8388608.f);
   lo = __fadd2_rn(make_float2(__uint_as_float(__byte_perm(w, 0x4B000000u, 0x7540u)),
@@ -380,9 +387,9 @@ resize_fast_kernel(FKParams kp, const vp_clip_plan* __restrict__ plans, const VI
               const float4 wa = w4t[y];                                                         \
               const float wb = w1t[y];                                                          \
               float2 fv[6];                   /* bytes (2q, 2q+1) as exact floats (PRMT + FADD2) */ \
-              bytes_to_f2(n0, fv[0], fv[1]);                                                    \
-              bytes_to_f2(n1, fv[2], fv[3]);                                                    \
-              bytes_to_f2(n2, fv[4], fv[5]);                                                    \
+              if (VP_CVT_I2F >= 1) bytes_to_f2_i2f(n0, fv[0], fv[1]); else bytes_to_f2(n0, fv[0], fv[1]); \
+              if (VP_CVT_I2F >= 2) bytes_to_f2_i2f(n1, fv[2], fv[3]); else bytes_to_f2(n1, fv[2], fv[3]); \
+              if (VP_CVT_I2F >= 3) bytes_to_f2_i2f(n2, fv[4], fv[5]); else bytes_to_f2(n2, fv[4], fv[5]); \
               const uint32_t used = rslot;                                                      \
               if (++rslot == kDepth) { rslot = 0; rphase ^= 1; }                                \
               if ((used & 3) == 3) {          /* group fully read: refill it */                 \
