@@ -172,13 +172,24 @@ struct FastCfg {
   static constexpr size_t OFF_WH = OFF_Y1 + (size_t)kOutHMax * 4;
   static constexpr size_t OFF_HX = OFF_WH + (size_t)kWhFloats * 4;
   static constexpr size_t OFF_BAR = (OFF_HX + (size_t)MAXWS * 4 + 15) & ~(size_t)15;
-  static constexpr size_t SMEM = OFF_BAR + (kNVW * kNGrp + 2 * (kCapR / 2)) * 8;
+  static constexpr size_t OFF_PROD = OFF_BAR + (kNVW * kNGrp + 2 * (kCapR / 2)) * 8;   // ProdState [kNVW]
+  static constexpr size_t SMEM = OFF_PROD + (size_t)kNVW * 32;
   static_assert(OFF_VBUF % 16 == 0 && OFF_WROW % 16 == 0 && OFF_WH % 16 == 0, "align");
 };
 
 // Per-V-warp TMA producer (lane 0): walks the CTA's item sequence and keeps its slice of kDepth rows
 // in flight.  issue() refills the slot of the row the warp has just finished reading.  The per-item
 // setup is a separate non-inlined function returning by value, so the per-row state stays in registers.
+// TMA producer state of one V warp, kept in shared memory (read/written once per 4-row refill) so that it
+// does not occupy registers in the register-bound V loop.
+struct ProdState {
+  const uint8_t* src;   // next source row of the slice
+  int64_t pitch;
+  int64_t next;         // next item to open
+  int rows, nbytes;     // rows left in the current item, bytes per row of the slice
+};
+static_assert(sizeof(ProdState) == 32, "ProdState");
+
 struct ProdItem {
   const uint8_t* src;   // this warp's slice of source row 0 of the item (nullptr: no more items)
   int64_t pitch;
@@ -277,40 +288,46 @@ resize_fast_kernel(FKParams kp, const vp_clip_plan* __restrict__ plans, const VI
     // TMA producer: warp-uniform state (every lane tracks it), copies / barrier ops predicated to lane 0,
     // so the refill is not a divergent branch.  A group of kGrp rows inside one item is one expect_tx.
     const bool l0 = lane == 0;
-    ProdItem pit = {nullptr, 0, my_a, 0, 0};
-    int64_t pnext = my_a;             // next item to open
-    const uint8_t* psrc = nullptr;
-    int prows = 0;
+    ProdState* ps = reinterpret_cast<ProdState*>(smem + Cfg::OFF_PROD) + warp;
+    if (l0) *ps = ProdState{nullptr, 0, my_a, 0, 0};
+    __syncwarp();
     auto issue_group = [&](uint32_t g) {          // refill the kGrp slots of group g, then arrive once
       // opaque copy of g (nvcc 12.9 CSE workaround, see vp_resize_ring.cu)
       asm volatile("mov.b32 %0, %0;" : "+r"(g));
-      if (prows >= kGrp) {
-        mbar_expect_tx_if(&full[g], (uint32_t)(kGrp * pit.nbytes), l0);
+      ProdState st = *ps;                         // warp-uniform (broadcast smem reads)
+      if (st.rows >= kGrp) {
+        mbar_expect_tx_if(&full[g], (uint32_t)(kGrp * st.nbytes), l0);
 #pragma unroll
         for (int q = 0; q < kGrp; ++q)
-          tma_bulk_g2s_if(stage + (size_t)(g * kGrp + q) * kWarpB, psrc + (int64_t)q * pit.pitch,
-                          (uint32_t)pit.nbytes, &full[g], l0 && pit.nbytes > 0);
-        psrc += (int64_t)kGrp * pit.pitch;
-        prows -= kGrp;
+          tma_bulk_g2s_if(stage + (size_t)(g * kGrp + q) * kWarpB, st.src + (int64_t)q * st.pitch,
+                          (uint32_t)st.nbytes, &full[g], l0 && st.nbytes > 0);
+        st.src += (int64_t)kGrp * st.pitch;
+        st.rows -= kGrp;
       } else {
 #pragma unroll 1
         for (int q = 0; q < kGrp; ++q) {
-          if (prows == 0 && pnext < my_b) {
-            pit = producer_open<VARIANT>(plans, vx, cnt, warp, frames, clip_off, pitch_arr, pnext, my_b);
-            ++pnext;
-            psrc = pit.src;
-            prows = pit.in_h;
+          if (st.rows == 0 && st.next < my_b) {
+            const ProdItem pit =
+                producer_open<VARIANT>(plans, vx, cnt, warp, frames, clip_off, pitch_arr, st.next, my_b);
+            ++st.next;
+            st.src = pit.src;
+            st.pitch = pit.pitch;
+            st.rows = pit.in_h;
+            st.nbytes = pit.nbytes;
           }
-          if (prows > 0) {
-            mbar_expect_tx_if(&full[g], (uint32_t)pit.nbytes, l0);
-            tma_bulk_g2s_if(stage + (size_t)(g * kGrp + q) * kWarpB, psrc, (uint32_t)pit.nbytes, &full[g],
-                            l0 && pit.nbytes > 0);
-            psrc += pit.pitch;
-            --prows;
+          if (st.rows > 0) {
+            mbar_expect_tx_if(&full[g], (uint32_t)st.nbytes, l0);
+            tma_bulk_g2s_if(stage + (size_t)(g * kGrp + q) * kWarpB, st.src, (uint32_t)st.nbytes, &full[g],
+                            l0 && st.nbytes > 0);
+            st.src += st.pitch;
+            --st.rows;
           }
         }
       }
       mbar_arrive_if(&full[g], l0);
+      __syncwarp();                               // every lane has read *ps
+      if (l0) *ps = st;
+      __syncwarp();
     };
     for (uint32_t g = 0; g < kNGrp; ++g) issue_group(g);     // prefill
     int64_t item = my_a;
