@@ -56,7 +56,8 @@ namespace {
 constexpr int kNVW = 4;                   // V warps
 constexpr int kNHW = 4;                   // H warps
 constexpr int kNT = (kNVW + kNHW) * 32;   // 256 threads
-constexpr int kDepth = 12;                // source rows in flight per V warp (refilled in groups of 4)
+constexpr int kDepth = 8;                 // source rows in flight per V warp (refilled in groups of 4)
+static_assert((kDepth & (kDepth - 1)) == 0, "the staging position is a masked running counter");
 constexpr int kGrp = 4;                   // rows per TMA group (one mbarrier phase per group)
 constexpr int kNGrp = kDepth / kGrp;
 constexpr int kWarpPx = 128;              // pixels per V warp slice (32 lanes x 4 px)
@@ -281,7 +282,7 @@ resize_fast_kernel(FKParams kp, const vp_clip_plan* __restrict__ plans, const VI
     asm volatile("setmaxnreg.inc.sync.aligned.u32 %0;\n" :: "n"(VP_VREGS) : "memory");
     uint8_t* stage = stage_all + (size_t)warp * kDepth * kWarpB;
     uint64_t* full = full_all + warp * kNGrp;     // one barrier per group of kGrp staging slots
-    uint32_t rslot = 0, rphase = 0;   // staging ring position of the next row to read
+    uint32_t rc = 0;                  // staged rows read so far: slot rc % kDepth, phase (rc / kDepth) & 1
     uint32_t vrow = 0;                // running count of retired rows
     uint32_t vslot = 0, vphase = 0;   // vbuf slot of the next retired row (= vrow % kCapR) and its pair phase
     int cached_clip = -1;
@@ -384,8 +385,8 @@ resize_fast_kernel(FKParams kp, const vp_clip_plan* __restrict__ plans, const VI
         // loading at the top of the row keeps the loop free of register rotation copies (measured faster).
         uint32_t n0 = 0, n1 = 0, n2 = 0;
         auto load_bytes = [&]() {
-          if ((rslot & (kGrp - 1)) == 0) mbar_wait(&full[rslot / kGrp], rphase);   // once per group
-          const uint32_t* sp = reinterpret_cast<const uint32_t*>(stage + rslot * kWarpB) + lane * 3;
+          if ((rc & (kGrp - 1)) == 0) mbar_wait(&full[(rc / kGrp) % kNGrp], (rc / kDepth) & 1);   // per group
+          const uint32_t* sp = reinterpret_cast<const uint32_t*>(stage + (rc % kDepth) * kWarpB) + lane * 3;
           n0 = sp[0]; n1 = sp[1]; n2 = sp[2];
         };
 
@@ -407,8 +408,7 @@ resize_fast_kernel(FKParams kp, const vp_clip_plan* __restrict__ plans, const VI
               if (VP_CVT_I2F >= 1) bytes_to_f2_i2f(n0, fv[0], fv[1]); else bytes_to_f2(n0, fv[0], fv[1]); \
               if (VP_CVT_I2F >= 2) bytes_to_f2_i2f(n1, fv[2], fv[3]); else bytes_to_f2(n1, fv[2], fv[3]); \
               if (VP_CVT_I2F >= 3) bytes_to_f2_i2f(n2, fv[4], fv[5]); else bytes_to_f2(n2, fv[4], fv[5]); \
-              const uint32_t used = rslot;                                                      \
-              if (++rslot == kDepth) { rslot = 0; rphase ^= 1; }                                \
+              const uint32_t used = rc++ % kDepth;                                              \
               if ((used & 3) == 3) {          /* group fully read: refill it */                 \
                 __syncwarp();                                                                   \
                 issue_group(used / kGrp);                                                       \
@@ -436,10 +436,9 @@ resize_fast_kernel(FKParams kp, const vp_clip_plan* __restrict__ plans, const VI
         }
         // source rows below the last window (none for the supported ratios) keep the ring in step
         for (; y < in_h; ++y) {
-          if ((rslot & (kGrp - 1)) == 0) mbar_wait(&full[rslot / kGrp], rphase);
+          if ((rc & (kGrp - 1)) == 0) mbar_wait(&full[(rc / kGrp) % kNGrp], (rc / kDepth) & 1);
           __syncwarp();
-          const uint32_t used = rslot;
-          if (++rslot == kDepth) { rslot = 0; rphase ^= 1; }
+          const uint32_t used = rc++ % kDepth;
           if ((used & 3) == 3) {
             __syncwarp();
             issue_group(used / kGrp);
