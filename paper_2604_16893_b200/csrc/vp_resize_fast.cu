@@ -283,8 +283,8 @@ resize_fast_kernel(FKParams kp, const vp_clip_plan* __restrict__ plans, const VI
     uint8_t* stage = stage_all + (size_t)warp * kDepth * kWarpB;
     uint64_t* full = full_all + warp * kNGrp;     // one barrier per group of kGrp staging slots
     uint32_t rc = 0;                  // staged rows read so far: slot rc % kDepth, phase (rc / kDepth) & 1
-    uint32_t vrow = 0;                // running count of retired rows
-    uint32_t vslot = 0, vphase = 0;   // vbuf slot of the next retired row (= vrow % kCapR) and its pair phase
+    uint32_t vslot = 0, vphase = 0;   // vbuf slot of the next retired row and its pair phase (kCapR even:
+                                      // vslot & 1 is the row's parity within its pair)
     int cached_clip = -1;
     // TMA producer: warp-uniform state (every lane tracks it), copies / barrier ops predicated to lane 0,
     // so the refill is not a divergent branch.  A group of kGrp rows inside one item is one expect_tx.
@@ -417,21 +417,19 @@ resize_fast_kernel(FKParams kp, const vp_clip_plan* __restrict__ plans, const VI
               if (!VP_EXP_NO_VMATH) ring_row<U>(acc, w5, fv);                                   \
             }                                                                                   \
             const uint32_t vs = vslot, vp2 = vs >> 1, vph = vphase;                             \
-            if ((vrow & 1) == 0 && !VP_EXP_NO_VWAIT) mbar_wait(&vempty[vp2], vph ^ 1);  /* per pair */ \
+            if ((vs & 1) == 0 && !VP_EXP_NO_VWAIT) mbar_wait(&vempty[vp2], vph ^ 1);    /* per pair */ \
             retire_slot<U>(acc, vbuf + vs * kRowPx, vb, vactive);                               \
             __syncwarp();                                                                       \
             if (lane == 0) mbar_arrive(&vfull[vp2]);                                            \
-            ++vrow;                                                                             \
             if (++vslot == kCapR) { vslot = 0; vphase ^= 1; }                                   \
           }
           static_assert(kRing == 5, "unroll below");
           VP_ROW(0) VP_ROW(1) VP_ROW(2) VP_ROW(3) VP_ROW(4)
 #undef VP_ROW
         }
-        if (vrow & 1) {                             // odd out_h: complete the last pair's barrier phase
+        if (vslot & 1) {                            // odd out_h: complete the last pair's barrier phase
           __syncwarp();
           if (lane == 0) mbar_arrive(&vfull[vslot >> 1]);
-          ++vrow;
           if (++vslot == kCapR) { vslot = 0; vphase ^= 1; }
         }
         // source rows below the last window (none for the supported ratios) keep the ring in step
