@@ -368,9 +368,10 @@ resize_fast_kernel(FKParams kp, const vp_clip_plan* __restrict__ plans, const VI
         named_sync(1, kNVW * 32);
         cached_clip = k;
       }
-      for (; item < cend && item < my_b; ++item) {
-        const int64_t local = item - cbase;
-        const Strip st = strip_of(pl, ws, (int)(local % nstrips));
+      // this clip's items in the slice as 32-bit local indices (fewer live 64-bit values in the row loop)
+      const int l_end = (int)((cend < my_b ? cend : my_b) - cbase);
+      for (int local = (int)(item - cbase); local < l_end; ++local) {
+        const Strip st = strip_of(pl, ws, local % nstrips);
         const int px_lane = warp * kWarpPx + lane * 4;      // this lane's first pixel (relative to pa)
         const bool vactive = px_lane < st.np;
         // vpos(px_lane + k) == vb + 8k for this lane's 4 pixels (px_lane is a multiple of 4)
@@ -443,6 +444,7 @@ resize_fast_kernel(FKParams kp, const vp_clip_plan* __restrict__ plans, const VI
           }
         }
       }
+      item = cbase + l_end;
     }
     return;
   }
