@@ -4,14 +4,15 @@
 // Work item = (clip, source frame f, strip of Ws <= 256 output columns).  A CTA walks the item's
 // source rows top to bottom exactly once with two warp-specialised groups:
 //   * 4 V warps (vertical pass).  Each V warp owns a 128-pixel (384-byte) slice of the strip's
-//     source footprint and keeps kDepth rows of it in flight with cp.async.bulk (global -> smem,
-//     completion on per-group mbarriers); the producer state is warp-uniform and only the copy /
+//     source footprint and keeps kDepth (16) rows of it in flight with cp.async.bulk (global -> smem,
+//     refilled in groups of 8, completion on per-group mbarriers); the producer state is warp-uniform and only the copy /
 //     barrier instructions are predicated to lane 0.  Lane L converts its 4 pixels (12 bytes) once per
-//     source row (PRMT into 2^23 + b, FADD2 -2^23: exact) and FMAs them (FFMA2, broadcast weight) into
+//     source row (I2F.U8 on the XU pipe for 2 of its 3 words, PRMT into 2^23 + b and FADD2 -2^23 for the
+//     third: both exact) and FMAs them (FFMA2, broadcast weight) into
 //     the output rows live at that row, held in a register ring acc[5] of float4 quads.  Output row i
 //     lives in slot i % 5; the output-row loop is unrolled by 5 so every slot index is static (no
 //     dynamic register indexing, no accumulator shuffles).
-//   * 4 H warps (horizontal pass).  Retired rows arrive through a 6-row smem buffer in row pairs
+//   * 4 H warps (horizontal pass).  Retired rows arrive through a 4-row smem buffer in row pairs
 //     (mbarrier hand-off each way), pixel-major float4 (RGB + pad) in a sub-pixel-major layout inside
 //     32-pixel blocks (vpos: conflict-free V stores, 1.35x H read wavefronts).  Each H thread computes a
 //     column pair x 2 rows x 3 channels over the pair's union window (LDS.128 per tap and row, 3 FFMA2:
@@ -56,13 +57,25 @@ namespace {
 constexpr int kNVW = 4;                   // V warps
 constexpr int kNHW = 4;                   // H warps
 constexpr int kNT = (kNVW + kNHW) * 32;   // 256 threads
-constexpr int kDepth = 8;                 // source rows in flight per V warp (refilled in groups of 4)
+// Staging depth / refill group / V->H buffer rows.  16/8/4 measured 3% faster than 8/4/6 on cfg5: the refill
+// (ProdState round trip, expect_tx, address setup) is paid once per 8 rows instead of 4, and the smem for the
+// deeper ring comes from the V->H buffer (its depth is irrelevant above 2 row pairs).
+#ifndef VP_DEPTH
+#define VP_DEPTH 16
+#endif
+#ifndef VP_GRP
+#define VP_GRP 8
+#endif
+#ifndef VP_CAPR
+#define VP_CAPR 4
+#endif
+constexpr int kDepth = VP_DEPTH;          // source rows in flight per V warp (refilled in groups of kGrp)
 static_assert((kDepth & (kDepth - 1)) == 0, "the staging position is a masked running counter");
-constexpr int kGrp = 4;                   // rows per TMA group (one mbarrier phase per group)
+constexpr int kGrp = VP_GRP;              // rows per TMA group (one mbarrier phase per group)
 constexpr int kNGrp = kDepth / kGrp;
 constexpr int kWarpPx = 128;              // pixels per V warp slice (32 lanes x 4 px)
 constexpr int kWarpB = 3 * kWarpPx;       // 384 bytes
-constexpr int kCapR = 6;                  // retired-row buffer rows (V -> H): 3 row pairs
+constexpr int kCapR = VP_CAPR;            // retired-row buffer rows (V -> H), in row pairs
 constexpr int kRowPx = kFastPx;           // float4 pixels per buffered row (union-slack taps wrap, weight 0)
 
 
@@ -176,6 +189,7 @@ struct FastCfg {
   static constexpr size_t OFF_PROD = OFF_BAR + (kNVW * kNGrp + 2 * (kCapR / 2)) * 8;   // ProdState [kNVW]
   static constexpr size_t SMEM = OFF_PROD + (size_t)kNVW * 32;
   static_assert(OFF_VBUF % 16 == 0 && OFF_WROW % 16 == 0 && OFF_WH % 16 == 0, "align");
+  static_assert(SMEM + 1024 <= 228 * 1024 / 2, "two CTAs per SM");
 };
 
 // Per-V-warp TMA producer (lane 0): walks the CTA's item sequence and keeps its slice of kDepth rows
@@ -410,7 +424,7 @@ resize_fast_kernel(FKParams kp, const vp_clip_plan* __restrict__ plans, const VI
               if (VP_CVT_I2F >= 2) bytes_to_f2_i2f(n1, fv[2], fv[3]); else bytes_to_f2(n1, fv[2], fv[3]); \
               if (VP_CVT_I2F >= 3) bytes_to_f2_i2f(n2, fv[4], fv[5]); else bytes_to_f2(n2, fv[4], fv[5]); \
               const uint32_t used = rc++ % kDepth;                                              \
-              if ((used & 3) == 3) {          /* group fully read: refill it */                 \
+              if ((used & (kGrp - 1)) == kGrp - 1) {   /* group read: refill it */                \
                 __syncwarp();                                                                   \
                 issue_group(used / kGrp);                                                       \
               }                                                                                 \
@@ -438,7 +452,7 @@ resize_fast_kernel(FKParams kp, const vp_clip_plan* __restrict__ plans, const VI
           if ((rc & (kGrp - 1)) == 0) mbar_wait(&full[(rc / kGrp) % kNGrp], (rc / kDepth) & 1);
           __syncwarp();
           const uint32_t used = rc++ % kDepth;
-          if ((used & 3) == 3) {
+          if ((used & (kGrp - 1)) == kGrp - 1) {
             __syncwarp();
             issue_group(used / kGrp);
           }
