@@ -511,7 +511,7 @@ resize_fast_kernel(FKParams kp, const vp_clip_plan* __restrict__ plans, const VI
       constexpr int kOffRegs = UL <= 11 ? UL : 1;
       int toff[kOffRegs];
 #pragma unroll
-      for (int u = 0; u < kOffRegs; ++u) toff[u] = vpos(xu + u);
+      for (int u = 0; u < kOffRegs; ++u) toff[u] = vpos(xu + u) * (int)sizeof(float4);   // byte offsets
       // column part of the output element index (O8): (wb*m^2 + mw)*D + px  (channel part added per c)
       int colpart;
       {
@@ -526,7 +526,21 @@ resize_fast_kernel(FKParams kp, const vp_clip_plan* __restrict__ plans, const VI
       const int64_t base0 = pl.patch_offset * (int64_t)kp.D + (int64_t)g0 * group_stride + (int64_t)ti0 * p * p;
       const int nslots = last_slot - f + 1;
       const int64_t hb_stride = (int64_t)(gw / m) * m * m * kp.D;
-      int r_hb = 0, r_mh = 0, r_py = 0;              // counters of the next row to emit
+      // element offset of the next row to emit (incl. this thread's column part), advanced per row:
+      // + p inside a patch row block, + d_mh when py wraps (next merge row), + d_hb when mh wraps too
+      // (32-bit offset from the frame's 64-bit base: one frame's patch block is < 2^31 elements)
+      const int64_t rbase = base0 + colpart;
+      int rp = 0, r_mh = 0, r_py = 0;
+      const int d_mh = m * kp.D - (p - 1) * p;
+      const int d_hb = (int)hb_stride - (m - 1) * m * kp.D - (p - 1) * p;
+      auto advance_row = [&]() {
+        if (++r_py == p) {
+          r_py = 0;
+          if (++r_mh == m) { r_mh = 0; rp += d_hb; } else rp += d_mh;
+        } else {
+          rp += p;
+        }
+      };
 
       for (int i = 0; i < out_h; i += 2) {
         const bool two = i + 1 < out_h;
@@ -535,13 +549,14 @@ resize_fast_kernel(FKParams kp, const vp_clip_plan* __restrict__ plans, const VI
           if (VP_H_SLEEP) mbar_wait_sleep(&vfull[s0 >> 1], ph0);
           else mbar_wait(&vfull[s0 >> 1], ph0);
         }
-        const int64_t rp0 = base0 + r_hb * hb_stride + (int64_t)(r_mh * m) * kp.D + r_py * p;
-        if (++r_py == p) { r_py = 0; if (++r_mh == m) { r_mh = 0; ++r_hb; } }
-        const int64_t rp1 = base0 + r_hb * hb_stride + (int64_t)(r_mh * m) * kp.D + r_py * p;
-        if (two) { if (++r_py == p) { r_py = 0; if (++r_mh == m) { r_mh = 0; ++r_hb; } } }
+        const int64_t rp0 = rbase + rp;
+        advance_row();
+        const int64_t rp1 = rbase + rp;
+        if (two) advance_row();
         if (writable && hact && !VP_EXP_NO_HMATH) {
-          const float4* v0 = vbuf + s0 * kRowPx;
-          const float4* v1 = vbuf + (two ? s1 : s0) * kRowPx;
+          // row bases (warp-uniform) + per-lane byte offsets: one LDS.128 [R + UR] per tap and row
+          const char* v0 = reinterpret_cast<const char*>(vbuf + s0 * kRowPx);
+          const char* v1 = reinterpret_cast<const char*>(vbuf + (two ? s1 : s0) * kRowPx);
           // accumulators per (channel, row) over the column pair (col a, col b): each tap is 3 FFMA2 per row,
           // the pixel's channel value broadcast against the pair's weights (w_a, w_b)
           float2 ar0 = make_float2(0.f, 0.f), ag0 = ar0, ab0 = ar0, ar1 = ar0, ag1 = ar0, ab1 = ar0;
@@ -549,8 +564,9 @@ resize_fast_kernel(FKParams kp, const vp_clip_plan* __restrict__ plans, const VI
 #pragma unroll
           for (int u = 0; u < UL; ++u) {
             const float2 wp = wr[u];                           // (col a, col b) weights at pixel xu+u
-            const int o = UL <= 11 ? toff[u < kOffRegs ? u : 0] : vpos(xu + u);
-            const float4 q0 = v0[o], q1 = v1[o];               // rows i, i+1
+            const int o = UL <= 11 ? toff[u < kOffRegs ? u : 0] : vpos(xu + u) * (int)sizeof(float4);
+            const float4 q0 = *reinterpret_cast<const float4*>(v0 + o);   // row i
+            const float4 q1 = *reinterpret_cast<const float4*>(v1 + o);   // row i + 1
             ar0 = __ffma2_rn(make_float2(q0.x, q0.x), wp, ar0);
             ag0 = __ffma2_rn(make_float2(q0.y, q0.y), wp, ag0);
             ab0 = __ffma2_rn(make_float2(q0.z, q0.z), wp, ab0);
@@ -584,23 +600,23 @@ resize_fast_kernel(FKParams kp, const vp_clip_plan* __restrict__ plans, const VI
           if (nslots == 1) {
             // common case: one temporal slot -> 3 (or 6) stores at constant channel offsets from a row pointer
             if (kF32) {
-              float* q0 = reinterpret_cast<float*>(pv) + rp0 + colpart;
+              float* q0 = reinterpret_cast<float*>(pv) + rp0;
               *reinterpret_cast<float2*>(q0) = xr0;
               *reinterpret_cast<float2*>(q0 + cstride) = xg0;
               *reinterpret_cast<float2*>(q0 + 2 * cstride) = xb0;
               if (two) {
-                float* q1 = reinterpret_cast<float*>(pv) + rp1 + colpart;
+                float* q1 = reinterpret_cast<float*>(pv) + rp1;
                 *reinterpret_cast<float2*>(q1) = xr1;
                 *reinterpret_cast<float2*>(q1 + cstride) = xg1;
                 *reinterpret_cast<float2*>(q1 + 2 * cstride) = xb1;
               }
             } else {
-              __nv_bfloat16* q0 = reinterpret_cast<__nv_bfloat16*>(pv) + rp0 + colpart;
+              __nv_bfloat16* q0 = reinterpret_cast<__nv_bfloat16*>(pv) + rp0;
               *reinterpret_cast<__nv_bfloat162*>(q0) = packbf(nr0, 0);
               *reinterpret_cast<__nv_bfloat162*>(q0 + cstride) = packbf(ng0, 1);
               *reinterpret_cast<__nv_bfloat162*>(q0 + 2 * cstride) = packbf(nb0, 2);
               if (two) {
-                __nv_bfloat16* q1 = reinterpret_cast<__nv_bfloat16*>(pv) + rp1 + colpart;
+                __nv_bfloat16* q1 = reinterpret_cast<__nv_bfloat16*>(pv) + rp1;
                 *reinterpret_cast<__nv_bfloat162*>(q1) = packbf(nr1, 0);
                 *reinterpret_cast<__nv_bfloat162*>(q1 + cstride) = packbf(ng1, 1);
                 *reinterpret_cast<__nv_bfloat162*>(q1 + 2 * cstride) = packbf(nb1, 2);
@@ -608,13 +624,13 @@ resize_fast_kernel(FKParams kp, const vp_clip_plan* __restrict__ plans, const VI
             }
           } else {
             // frame n-1 of a clip also fills the temporal pad slots (O7), images fill tp slots
-            store_slots<kF32>(pv, rp0 + colpart, xr0a, xr0b, nslots, ti0, tp, p, group_stride);
-            store_slots<kF32>(pv, rp0 + colpart + cstride, xg0a, xg0b, nslots, ti0, tp, p, group_stride);
-            store_slots<kF32>(pv, rp0 + colpart + 2 * cstride, xb0a, xb0b, nslots, ti0, tp, p, group_stride);
+            store_slots<kF32>(pv, rp0, xr0a, xr0b, nslots, ti0, tp, p, group_stride);
+            store_slots<kF32>(pv, rp0 + cstride, xg0a, xg0b, nslots, ti0, tp, p, group_stride);
+            store_slots<kF32>(pv, rp0 + 2 * cstride, xb0a, xb0b, nslots, ti0, tp, p, group_stride);
             if (two) {
-              store_slots<kF32>(pv, rp1 + colpart, xr1a, xr1b, nslots, ti0, tp, p, group_stride);
-              store_slots<kF32>(pv, rp1 + colpart + cstride, xg1a, xg1b, nslots, ti0, tp, p, group_stride);
-              store_slots<kF32>(pv, rp1 + colpart + 2 * cstride, xb1a, xb1b, nslots, ti0, tp, p, group_stride);
+              store_slots<kF32>(pv, rp1, xr1a, xr1b, nslots, ti0, tp, p, group_stride);
+              store_slots<kF32>(pv, rp1 + cstride, xg1a, xg1b, nslots, ti0, tp, p, group_stride);
+              store_slots<kF32>(pv, rp1 + 2 * cstride, xb1a, xb1b, nslots, ti0, tp, p, group_stride);
             }
           }
         }
