@@ -16,20 +16,21 @@ from parity import assert_pixels, host_frames, oracle_params, pack_frames
 pytestmark = pytest.mark.gpu
 
 
-def _gpu_run(pre, clips, kind="noise", pitch_pad=0, frames=None):
+def _gpu_run(pre, clips, kind="noise", pitch_pad=0, frames=None, align16=False):
     pl = pre.plan(clips)
     op = oracle_params(pre.params)
     oplans, _ = O.plan_batch(op, clips)
     fl = host_frames(oplans, kind) if frames is None else frames
-    pitches = [3 * c["width"] + pitch_pad for c in clips]
+    # 16-B aligned pitches (and hence offsets) let the TMA variants take the clip; otherwise it is generic
+    pitches = [(3 * c["width"] + 15) // 16 * 16 if align16 else 3 * c["width"] + pitch_pad for c in clips]
     buf, offs, pit = pack_frames(fl, pitches)
     out = pre.run(pl, buf, offs, pit)
     torch.cuda.synchronize()
     return pl, oplans, fl, out
 
 
-def _full_compare(pre, clips, kind="noise", pitch_pad=0):
-    pl, oplans, fl, out = _gpu_run(pre, clips, kind, pitch_pad)
+def _full_compare(pre, clips, kind="noise", pitch_pad=0, align16=False):
+    pl, oplans, fl, out = _gpu_run(pre, clips, kind, pitch_pad, align16=align16)
     op = oracle_params(pre.params)
     ref = O.process_batch(op, clips, [f if f is not None else np.zeros((1, 1, 1, 3), np.uint8) for f in fl],
                           plans=oplans)
@@ -66,8 +67,11 @@ def test_small_mixed_ragged_batch(dtype):
     _full_compare(pre, clips)
 
 
+@pytest.mark.parametrize("align16", [False, True])
 @pytest.mark.parametrize("seed", range(4))
-def test_random_shapes_and_pitches(seed):
+def test_random_shapes_and_pitches(seed, align16):
+    """Random geometry and model params; unaligned pitches route clips to the generic kernel, 16-B aligned
+    ones to the TMA fast / copy variants."""
     import paper_2604_16893_b200 as vp
     rng = random.Random(100 + seed)
     tp = rng.choice([1, 2, 3])
@@ -79,7 +83,7 @@ def test_random_shapes_and_pitches(seed):
     for _ in range(rng.randint(1, 6)):
         h, w = rng.randint(8, 600), rng.randint(8, 600)
         clips.append(I.image(h, w) if rng.random() < 0.4 else I.clip(rng.randint(1, 40), rng.choice([2.0, 5.0]), h, w))
-    _full_compare(pre, clips, pitch_pad=rng.choice([0, 1, 5, 16]))
+    _full_compare(pre, clips, pitch_pad=rng.choice([0, 1, 5, 16]), align16=align16)
 
 
 @pytest.mark.parametrize("dtype", [1, 0])
@@ -178,9 +182,9 @@ def test_cfg2_one_clip_full():
     _full_compare(vp.VisualPreprocessor(**params), clips)
 
 
-def _sampled_compare(pre, clips, n_samples=4000, seed=0, kind="noise"):
+def _sampled_compare(pre, clips, n_samples=4000, seed=0, kind="noise", align16=False):
     """Full-size launch; the oracle computes sampled outputs one by one (resize_pixel)."""
-    pl, oplans, fl, out = _gpu_run(pre, clips, kind)
+    pl, oplans, fl, out = _gpu_run(pre, clips, kind, align16=align16)
     op = oracle_params(pre.params)
     p, m, tp = op["patch_size"], op["merge_size"], op["temporal_patch_size"]
     rng = np.random.default_rng(seed)
@@ -216,6 +220,24 @@ def test_cfg4_sampled():
     import paper_2604_16893_b200 as vp
     params, clips = I.config("cfg4")
     _sampled_compare(vp.VisualPreprocessor(**params), clips, n_samples=3000)
+
+
+def test_fast_groups_straddle_items():
+    """The fast kernel's TMA staging refills in groups of 8 source rows; when a source height is not a
+    multiple of 8 a group straddles two work items (the per-row refill path that opens the next item).
+    40 odd-height clips x 16 frames = 640 items over 2 CTAs/SM x 148 SMs, so every CTA walks several
+    consecutive items of different heights; sampled outputs of every clip against the oracle."""
+    import paper_2604_16893_b200 as vp
+    rng = random.Random(7)
+    pre = vp.VisualPreprocessor(max_frames=16, video_max_pixels=100000, out_dtype=1)   # ratios ~1.1-2.1
+    clips = []
+    while len(clips) < 40:
+        h, w = rng.randint(300, 520), rng.randint(380, 700)
+        if h % 8:
+            clips.append(I.clip(240, 30.0, h, w))
+    kv = pre.plan(clips).plans_host["kernel_variant"][:len(clips)]
+    assert all(v in (0, 1, 2) for v in kv) and sum(v == 0 for v in kv) >= 30, kv   # fast variants, mostly MILD
+    _sampled_compare(pre, clips, n_samples=6000, seed=3, align16=True)
 
 
 def test_cfg5_bench_launch_sampled():
