@@ -136,7 +136,7 @@ def run_ours(args, rank, world, local_rank):
         vp.synth_frames(vp.VP_SYNTH_NOISE, 1000003 * 0 + rank * per + k, ids, H, W, frames[off[k]:], int(pitch[k]))
     off_d = torch.from_numpy(off).to(dev)
     pitch_d = torch.from_numpy(pitch).to(dev)
-    out = pre.alloc_outputs(pl)
+    out = pre.alloc_outputs(pl)            # includes the K3 workspace (caller-owned scratch)
     # token-type sequences: one sequence per clip (Qwen3-VL: "<t s><vision_start> group <vision_end>" per group)
     seqs = []
     for k in range(per):
@@ -182,7 +182,7 @@ def run_ours(args, rank, world, local_rank):
         vp.resize_normalize_patchify(P, pl.plans_dev, per, frames, off_d, pitch_d,
                                      out["pixel_values"] if n_img else None,
                                      out["pixel_values_videos"], out["image_grid_thw"], out["video_grid_thw"],
-                                     out["clip_status"])
+                                     out["clip_status"], workspace=out["workspace"])
         if record:
             b.record(stream)
             ev_k3.append((a, b))
@@ -245,7 +245,7 @@ def run_ours(args, rank, world, local_rank):
                        "parallelism": f"clip-sharded dp{world}"},
             "hbm_gbs_step": k3_bytes / (ms_step * 1e-3) / 1e9,
             "roofline": {"bound": "hbm", "achieved": achieved, "peak": peak, "unit": "GB/s",
-                         "frac": achieved / peak, "traffic": traffic, "kernel": "vp_resize_normalize_patchify (K3: resize_fast_kernel, fused AA-bicubic resize/normalise/patchify)",
+                         "frac": achieved / peak, "traffic": traffic, "kernel": "vp_resize_normalize_patchify (K3: resize_team_kernel, fused AA-bicubic resize/normalise/patchify)",
                          "k3_ms": k3_ms, "algorithmic_bytes_per_launch": k3_bytes, "peak_source": peak_src},
             "gpu_launches": launches_per_step * args.steps,
             "clocks": clk,
@@ -285,6 +285,7 @@ def run_e2e(args, pre, pl, frames, off, pitch, out, tt, cu, pos, deltas, rst, ws
     comp = torch.cuda.current_stream(dev)
     copy = torch.cuda.Stream(dev)
     h2d = per * clip_bytes
+    ws_chunk = vp.resize_workspace(chunk, dev)
     d2h = grids_h.numel() * 8 + st_h.numel() * 4 + dl_h.numel() * 8 + rs_h.numel() * 4
 
     def step():
@@ -305,7 +306,7 @@ def run_e2e(args, pre, pl, frames, off, pitch, out, tt, cu, pos, deltas, rst, ws
             comp.wait_event(e)
             vp.resize_normalize_patchify(P, pl.plans_dev, c1 - c0, frames, torch_off, torch_pitch, None,
                                          out["pixel_values_videos"], out["image_grid_thw"], out["video_grid_thw"],
-                                         out["clip_status"], stream=comp, first_clip=c0)
+                                         out["clip_status"], workspace=ws_chunk, stream=comp, first_clip=c0)
             d = torch.cuda.Event()
             d.record(comp)
             done.append(d)

@@ -10,7 +10,9 @@
  *
  * Conventions for every entry point
  *   - All array arguments marked (dev) are device pointers owned by the caller; the library never
- *     allocates device memory and keeps no state between calls (reentrant).
+ *     allocates device memory (scratch is a caller-provided workspace) and keeps no state between calls
+ *     beyond idempotent per-device caches (SM count, kernel shared-memory attributes), so calls are
+ *     reentrant and thread-safe on any device and stream.
  *   - Work is enqueued on `stream` (a cudaStream_t, passed as void*; NULL = legacy default stream);
  *     no call synchronises the device, so every call is CUDA-graph capturable.
  *   - The return value reports host-detectable errors synchronously (null pointers, invalid
@@ -166,15 +168,19 @@ vp_status vp_plan_frames(const vp_params* p, const vp_clip_desc* clips, int32_t 
  *   clip_status (dev, nullable) [n] int32 output: VP_OK, VP_EINVAL (invalid plan), VP_ECAPACITY
  *                      (rows beyond the cap; that clip's rows are not written) or VP_EUNSUPPORTED
  *                      (a per-axis downscale beyond ~34x; that clip's rows are not written)
- * Errors: VP_EINVAL, VP_EUNSUPPORTED, VP_ECUDA.
+ *   workspace (dev)    vp_resize_workspace_bytes(n) bytes, 256-B aligned, caller-owned scratch (work index and
+ *                      per-clip weight tables, rebuilt on every call; contents need not persist)
+ * Errors: VP_EINVAL (incl. a missing / short / misaligned workspace), VP_EUNSUPPORTED, VP_ECUDA.
  * ------------------------------------------------------------------------------------------- */
+size_t vp_resize_workspace_bytes(int32_t n);
 vp_status vp_resize_normalize_patchify(const vp_params* p, const vp_clip_plan* plans, int32_t n,
                                        const uint8_t* frames,
                                        const int64_t* clip_byte_offset, const int64_t* row_pitch,
                                        void* pixel_values_images, int64_t img_rows_cap,
                                        void* pixel_values_videos, int64_t vid_rows_cap,
                                        int64_t* image_grid_thw, int64_t* video_grid_thw,
-                                       int32_t* clip_status, void* stream);
+                                       int32_t* clip_status, void* workspace, size_t workspace_bytes,
+                                       void* stream);
 
 /* ---------------------------------------------------------------------------------------------
  * vp_rope_index -- H8: 3D MRoPE position ids for a packed (padding-free) batch of B

@@ -19,7 +19,8 @@ from ._lib import (DESC_DTYPE, PLAN_DTYPE, TOT, TOT_LEN, VP_BUDGET_PER_FRAME, VP
                    check, lib)
 
 __all__ = [
-    "make_params", "clip_desc_array", "plan_frames", "resize_normalize_patchify", "rope_index",
+    "make_params", "clip_desc_array", "plan_frames", "resize_normalize_patchify", "resize_workspace_bytes",
+    "resize_workspace", "rope_index",
     "rope_index_workspace_bytes", "plan_records", "pack_offsets", "synth_frames", "VisualPreprocessor",
     "PlacementMismatch", "VpError", "VpParams", "DESC_DTYPE", "PLAN_DTYPE", "TOT", "TOT_LEN",
     "VP_ROPE_QWEN3_SPLIT", "VP_ROPE_QWEN2", "VP_ROPE_QWEN25", "VP_OUT_BF16", "VP_OUT_F32",
@@ -78,10 +79,20 @@ def plan_frames(params: VpParams, clips, n: int, plans, frame_indices, totals, g
                              _stream(stream)), "vp_plan_frames")
 
 
+def resize_workspace_bytes(n: int) -> int:
+    return int(lib.vp_resize_workspace_bytes(int(n)))
+
+
+def resize_workspace(n: int, device) -> torch.Tensor:
+    """Caller-owned scratch for vp_resize_normalize_patchify (256-B aligned by the torch allocator)."""
+    return torch.empty(max(resize_workspace_bytes(n), 256), dtype=torch.uint8, device=device)
+
+
 def resize_normalize_patchify(params: VpParams, plans, n: int, frames, clip_byte_offset, row_pitch,
                               pixel_values_images, pixel_values_videos, image_grid_thw, video_grid_thw,
-                              clip_status=None, stream=None, first_clip: int = 0) -> None:
-    """vp_resize_normalize_patchify (O4-O9) for clips [first_clip, first_clip+n) of a plan array."""
+                              clip_status=None, workspace=None, stream=None, first_clip: int = 0) -> None:
+    """vp_resize_normalize_patchify (O4-O9) for clips [first_clip, first_clip+n) of a plan array.
+    ``workspace``: uint8 device tensor of >= resize_workspace_bytes(n) bytes (allocated here if None)."""
     D = 3 * params.temporal_patch_size * params.patch_size ** 2
     icap = pixel_values_images.numel() // D if pixel_values_images is not None else 0
     vcap = pixel_values_videos.numel() // D if pixel_values_videos is not None else 0
@@ -90,10 +101,13 @@ def resize_normalize_patchify(params: VpParams, plans, n: int, frames, clip_byte
     co = clip_byte_offset.data_ptr() + 8 * k0
     rp = row_pitch.data_ptr() + 8 * k0
     cs = clip_status.data_ptr() + 4 * k0 if clip_status is not None else None
+    if workspace is None:
+        workspace = resize_workspace(n, frames.device)
     check(lib.vp_resize_normalize_patchify(C.byref(params), pp, int(n), _ptr(frames), co, rp,
                                            _ptr(pixel_values_images),
                                            icap, _ptr(pixel_values_videos), vcap, _ptr(image_grid_thw),
-                                           _ptr(video_grid_thw), cs, _stream(stream)),
+                                           _ptr(video_grid_thw), cs, _ptr(workspace), workspace.numel(),
+                                           _stream(stream)),
           "vp_resize_normalize_patchify")
 
 
@@ -183,8 +197,10 @@ class VisualPreprocessor:
         pl.plans_host = pl.plans_dev.cpu().numpy()[: pl.n * PLAN_DTYPE.itemsize].view(PLAN_DTYPE).copy()
         return pl
 
-    def frames_layout(self, pl: Plan, row_align: int = 1):
-        """Packed layout of every valid clip's sampled frames: (clip_byte_offset, row_pitch, total bytes)."""
+    def frames_layout(self, pl: Plan, row_align: int = 16):
+        """Packed layout of every valid clip's sampled frames: (clip_byte_offset, row_pitch, total bytes).
+        Rows are padded to 16 B by default so every clip can take the TMA kernels (unaligned rows fall back to
+        the generic kernel)."""
         ph = pl.plans_host
         off = np.zeros(pl.n, dtype=np.int64)
         pitch = np.zeros(pl.n, dtype=np.int64)
@@ -205,18 +221,23 @@ class VisualPreprocessor:
             image_grid_thw=torch.empty(t["n_images"], 3, dtype=torch.int64, device=self.device),
             video_grid_thw=torch.empty(t["n_videos"], 3, dtype=torch.int64, device=self.device),
             clip_status=torch.empty(max(pl.n, 1), dtype=torch.int32, device=self.device),
+            workspace=resize_workspace(pl.n, self.device),
         )
 
     # -- H5-H7 --
-    def run(self, pl: Plan, frames, clip_byte_offset, row_pitch, out=None, stream=None, strict=False):
+    def run(self, pl: Plan, frames, clip_byte_offset, row_pitch, out=None, stream=None, strict=True):
+        """Strict by default: a clip whose rows the kernels could not write (VP_ECAPACITY,
+        VP_EUNSUPPORTED) raises.  Clips with invalid descriptors are recorded as VP_EINVAL in
+        ``clip_status`` / the plan without aborting the batch."""
         out = self.alloc_outputs(pl) if out is None else out
         resize_normalize_patchify(self.params, pl.plans_dev, pl.n, frames, clip_byte_offset,
                                   row_pitch, out["pixel_values"] if out["pixel_values"].numel() else None,
                                   out["pixel_values_videos"] if out["pixel_values_videos"].numel() else None,
-                                  out["image_grid_thw"], out["video_grid_thw"], out["clip_status"], stream=stream)
+                                  out["image_grid_thw"], out["video_grid_thw"], out["clip_status"],
+                                  workspace=out.get("workspace"), stream=stream)
         if strict:
             st = out["clip_status"][: pl.n].cpu().numpy()
-            bad = np.nonzero(st)[0]
+            bad = np.nonzero((st != VP_OK) & (st != VP_EINVAL))[0]
             if len(bad):
                 raise VpError(int(st[bad[0]]), f"clip {int(bad[0])}")
         return out

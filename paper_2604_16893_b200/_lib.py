@@ -24,7 +24,7 @@ TOT = dict(indices=0, img_rows=1, vid_rows=2, img_tokens=3, vid_tokens=4, n_imag
            vid_groups=7, tiles=8, flags=9, n_invalid=10)
 TOT_LEN = 12
 
-EXPORTED = ["vp_plan_frames", "vp_resize_normalize_patchify", "vp_rope_index_workspace_bytes", "vp_rope_index",
+EXPORTED = ["vp_plan_frames", "vp_resize_workspace_bytes", "vp_resize_normalize_patchify", "vp_rope_index_workspace_bytes", "vp_rope_index",
             "vp_pack_offsets", "vp_plan_records", "vp_synth_frames", "vp_status_string", "vp_last_error_detail",
             "vp_abi_version", "vp_struct_sizes"]
 
@@ -57,7 +57,8 @@ def _load() -> C.CDLL:
     P = C.POINTER(VpParams)
     sig = {
         "vp_plan_frames": (i32, [P, vp, i32, vp, vp, i64, vp, i64, vp, vp]),
-        "vp_resize_normalize_patchify": (i32, [P, vp, i32, vp, vp, vp, vp, i64, vp, i64, vp, vp, vp, vp]),
+        "vp_resize_workspace_bytes": (sz, [i32]),
+        "vp_resize_normalize_patchify": (i32, [P, vp, i32, vp, vp, vp, vp, i64, vp, i64, vp, vp, vp, vp, sz, vp]),
         "vp_rope_index_workspace_bytes": (sz, [i32, i32]),
         "vp_rope_index": (i32, [P, i32, vp, vp, i32, i64, vp, i32, vp, i32, vp, i32, vp, vp, vp, vp, sz, vp]),
         "vp_pack_offsets": (i32, [vp, i32, i32, vp, vp, vp]),

@@ -50,7 +50,7 @@ constexpr int kTotLen = VP_TOT_LEN;
 // KV_GENERIC covers everything else (vp_resize.cu, token tiles).  A clip's items (tile_count)
 // are n_frames x n_strips for the fast variants, 0 for generic.  Integer / f64 exact.
 // ------------------------------------------------------------------------------------------
-enum { KV_MILD = 0, KV_MEDIUM = 1, KV_STRONG = 2, KV_GENERIC = 3, KV_COPY = 4, KV_RING = 5 };
+enum { KV_MILD = 0, KV_MEDIUM = 1, KV_STRONG = 2, KV_GENERIC = 3, KV_COPY = 4, KV_TEAM = 5 };
 constexpr int kRing = 5;          // vertical ring slots: max live output rows per source row for in/out > 0.8
 constexpr int kInHMax = 1088;     // source rows supported by the fast kernel's per-row weight table
 constexpr int kWListMax = 6144;   // vertical weights (sum of window lengths) held in smem
@@ -97,35 +97,56 @@ __host__ __device__ __forceinline__ int fast_strip_width(int in_w, int out_w) {
 constexpr int kCopyMW = 8;
 __host__ __device__ __forceinline__ int copy_wchunks(int grid_w, int m) { return (grid_w / m + kCopyMW - 1) / kCopyMW; }
 
-// KV_RING (vp_resize_ring.cu): one warp per CTA streams a (clip, strip, frame) item through a vertical
-// register ring (lanes = 4 source pixels, <= kRingPx footprint pixels per strip) and a horizontal ring
-// (lanes = output rows).  Both axes must be downscales or identity (in >= out): then at most 5 output rows
-// (columns) are live per source row (pixel), see DESIGN.md.  The strip width is the largest multiple of 8
-// whose footprint, started at a 4-pixel boundary, fits kRingPx:  3 + (Ws-1)*s + 2*(2*fs) + 2 <= kRingPx.
-// Strips narrower than kRingMinWs would re-read too much halo; those clips use the other variants.
-constexpr int kRingPx = 120;      // 30 lanes x 4 px
-constexpr int kRingMaxWs = 64;
-constexpr int kRingMinWs = 32;
-constexpr int kRingInHMax = 2176; // per-clip vertical table rows (ring_vtables_kernel slot size)
-__host__ __device__ __forceinline__ int ring_strip_width(int in_w, int out_w) {
-  if (in_w < out_w) return 0;
+// KV_TEAM (vp_resize_team.cu): a CTA of kTeamW warps walks one (clip, slice, frame) item; every warp does the
+// vertical ring on a 128-pixel part of the slice footprint and the horizontal pass of its column pairs.  Needs a
+// downscale or identity on both axes (then <= 4 output rows are live per source row), an even
+// patch size (bf16x2 / float2 column pairs), a horizontal union window (column pair) of <= kTeamUL taps and the
+// per-clip tables (kTabInH source rows, kTabOutH output rows).  Slices are multiples of p columns (each patch row
+// is written by one CTA: no partially written sectors shared between CTAs) of <= 64*kTeamW columns whose footprint
+// fits 128*kTeamW pixels; the slice count is balanced.  Items per clip: n_frames x nslices.
+constexpr int kTeamW = 4;         // warps per team CTA
+constexpr int kTeamUL = 10;       // union taps of a column pair (registers)
+constexpr int kTabInH = 1088;     // per-clip vertical weight records (float4 per source row)
+constexpr int kTabOutH = 1088;    // per-clip window ends (int per output row, padded to a multiple of 4)
+
+struct TeamGeo {
+  int ws, nslices;                // slice width (columns), slices per frame; ws = 0: does not fit
+};
+__host__ __device__ __forceinline__ TeamGeo team_geometry(int in_w, int out_w, int p) {
+  TeamGeo g{0, 0};
+  if (p < 2 || (p & 1) || out_w < p) return g;
   const double s = (double)in_w / (double)out_w;
-  int best = 0;
-  for (int ws = 8; ws <= kRingMaxWs; ws += 8)
-    if (3.0 + (ws - 1) * s + 4.0 * s + 2.0 <= (double)kRingPx) best = ws;
-  if (best > out_w) best = out_w;
-  return best;
+  const double fs = s > 1.0 ? s : 1.0;
+  // footprint of c consecutive columns from a 4-pixel aligned start: < (c-1)*s + 4*fs + 1 + 3 pixels
+  int cmax = 0;
+  for (int c = p; c <= 64 * kTeamW && c <= out_w; c += p)
+    if ((c - 1) * s + 4.0 * fs + 4.0 + 0.01 <= 128.0 * kTeamW) cmax = c;
+  if (cmax == 0) return g;
+  const int n = (out_w + cmax - 1) / cmax;
+  int ws = (out_w + n - 1) / n;
+  ws = (ws + p - 1) / p * p;
+  if (ws > cmax) ws = cmax;
+  g.ws = ws;
+  g.nslices = (out_w + ws - 1) / ws;
+  return g;
+}
+// taps of the union of two adjacent columns' windows: x1(j+1) - x0(j) < s + 4*fs + 1
+__host__ __device__ __forceinline__ int pair_union_bound(int in, int out) {
+  const double s = (double)in / (double)out;
+  const double fs = s > 1.0 ? s : 1.0;
+  return (int)floor(s + 4.0 * fs + 1.0 + 1e-9);
 }
 
-__host__ __device__ __forceinline__ int select_variant(int in_h, int in_w, int out_h, int out_w, int p, int ring) {
+__host__ __device__ __forceinline__ int select_variant(int in_h, int in_w, int out_h, int out_w, int p) {
   if (in_h == out_h && in_w == out_w && (p & 1) == 0) return KV_COPY;
-  if (ring && in_h >= out_h && in_h <= kRingInHMax && p == 16 && ring_strip_width(in_w, out_w) >= kRingMinWs &&
-      out_w % 8 == 0)
-    return KV_RING;
+  if (in_h >= out_h && in_w >= out_w && (p & 1) == 0 && in_h <= kTabInH && out_h <= kTabOutH &&
+      pair_union_bound(in_w, out_w) <= kTeamUL && team_geometry(in_w, out_w, p).ws > 0)
+    return KV_TEAM;
   const double sv = (double)in_h / (double)out_h;
   // live output rows per source row <= floor(4/s)+1 for upscale (<= 5 iff s > 0.8) and <= 5 for downscale
-  // (trimmed windows; brute-forced in tests/test_oracle_pixels.py::test_live_rows_bound)
-  if (!(sv > 0.8) || in_h > kInHMax || out_h > kOutHMax) return KV_GENERIC;
+  // (trimmed windows; brute-forced in tests/test_oracle_pixels.py::test_live_rows_bound).  The streaming kernel
+  // stores column pairs (bf16x2 / float2), so it needs an even patch size.
+  if ((p & 1) || !(sv > 0.8) || in_h > kInHMax || out_h > kOutHMax) return KV_GENERIC;
   const double sh = (double)in_w / (double)out_w;
   if (sh < 0.6 || fast_strip_width(in_w, out_w) < 16) return KV_GENERIC;
   const int th = axis_max_taps(in_w, out_w);

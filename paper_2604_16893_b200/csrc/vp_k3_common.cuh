@@ -1,4 +1,4 @@
-// vp_k3_common.cuh -- device helpers shared by the K3 kernels (vp_resize_fast.cu, vp_resize_ring.cu):
+// vp_k3_common.cuh -- device helpers shared by the K3 kernels (vp_resize_fast.cu, vp_resize_team.cu, vp_resize.cu):
 // normalisation parameters, mbarrier / TMA-bulk PTX wrappers, the AA-bicubic window (C10) and the
 // per-variant work index.  Private to the CUDA path; nothing here is shared with oracle/.
 #pragma once
@@ -18,6 +18,21 @@ struct FKParams {
 // ---------------------------------------------------------------- PTX helpers (mbarrier / TMA bulk)
 __device__ __forceinline__ uint32_t smem_u32(const void* p) {
   return static_cast<uint32_t>(__cvta_generic_to_shared(p));
+}
+// Shared-memory accesses at explicit 32-bit shared addresses (volatile: ordered with the mbarrier waits / barriers
+// that guard the data; the address arithmetic folds into [R + imm] with no generic-to-shared conversion).
+__device__ __forceinline__ uint32_t lds_u32(uint32_t a) {
+  uint32_t v;
+  asm volatile("ld.shared.u32 %0, [%1];" : "=r"(v) : "r"(a));
+  return v;
+}
+__device__ __forceinline__ float4 lds_f4(uint32_t a) {
+  float4 v;
+  asm volatile("ld.shared.v4.f32 {%0, %1, %2, %3}, [%4];" : "=f"(v.x), "=f"(v.y), "=f"(v.z), "=f"(v.w) : "r"(a));
+  return v;
+}
+__device__ __forceinline__ void sts_f4(uint32_t a, float4 v) {
+  asm volatile("st.shared.v4.f32 [%0], {%1, %2, %3, %4};" ::"r"(a), "f"(v.x), "f"(v.y), "f"(v.z), "f"(v.w) : "memory");
 }
 __device__ __forceinline__ void mbar_init(uint64_t* bar, uint32_t count) {
   asm volatile("mbarrier.init.shared::cta.b64 [%0], %1;" ::"r"(smem_u32(bar)), "r"(count));
@@ -135,14 +150,32 @@ __device__ __forceinline__ int vfind(const VIdx& vx, int cnt, int64_t item) {   
   return lo;
 }
 
-// Per-variant work-index slots (variant_index_kernel): MILD, MEDIUM, STRONG, COPY, RING.
+// Per-variant work-index slots (variant_index_kernel): MILD, MEDIUM, STRONG, COPY, TEAM.
 constexpr int kNSlots = 5;
 
-// KV_RING launcher (vp_resize_ring.cu).  vt = per-clip vertical tables (ring_vtables_kernel), vt_owner[j] =
-// list position whose table clip j of the ring list uses.
-cudaError_t launch_resize_ring(const FKParams& kp, const vp_clip_plan* plans, const VIdx& vx, const uint8_t* frames,
-                               const int64_t* coff, const int64_t* pitch, void* pi, int64_t icap, void* pvv,
-                               int64_t vcap, int n, void* vt, int* vt_owner, int num_sms, cudaStream_t s);
-size_t ring_vtable_bytes();
+// Caller workspace of vp_resize_normalize_patchify (resize_ws_layout): the per-variant work index and the
+// KV_TEAM per-clip tables.  Nothing persists between calls.
+struct ResizeWs {
+  size_t bytes;
+  int* list;          // [kNSlots][n]
+  int64_t* off;       // [kNSlots][n+1]
+  int64_t* meta;      // [kNSlots][2]
+  int* alias;         // [n]  TEAM list position -> table owner
+  int* tflag;         // [n]  table flags (a non-negligible 5th live row)
+  float4* vtab;       // [n][kTabInH]
+  int* y1tab;         // [n][kTabOutH]
+};
+ResizeWs resize_ws_layout(int n, void* base);
+VIdx ws_vidx(const ResizeWs& w, int n, int slot);
+int device_sms(int dev);
+cudaError_t launch_index(const vp_clip_plan* plans, int n, const int64_t* coff, const int64_t* pitch,
+                         const ResizeWs& w, cudaStream_t s);
+cudaError_t launch_team(const FKParams& kp, const vp_clip_plan* plans, int n, const ResizeWs& w, const uint8_t* frames,
+                        const int64_t* coff, const int64_t* pitch, void* pi, int64_t icap, void* pvv, int64_t vcap,
+                        int32_t* clip_status, int num_sms, cudaStream_t s);
+cudaError_t launch_fast_variants(const FKParams& kp, const vp_clip_plan* plans, int n, const ResizeWs& w,
+                                 const uint8_t* frames, const int64_t* coff, const int64_t* pitch, void* pi,
+                                 int64_t icap, void* pvv, int64_t vcap, int dev, int num_sms, cudaStream_t s);
+FKParams make_fkparams(const vp_params* p);
 
 }  // namespace vp

@@ -9,7 +9,6 @@
 // intrinsics (__ddiv_rn/__dmul_rn/__dsqrt_rn/__dadd_rn) in the order the definition states,
 // and this TU is compiled with --fmad=false, so the results equal IEEE evaluation on the host.
 #include "vp_internal.cuh"
-#include <cstdlib>
 
 namespace vp {
 namespace {
@@ -98,7 +97,7 @@ __device__ __forceinline__ int64_t frame_index(int64_t i, int64_t total, int64_t
 __global__ void __launch_bounds__(kPlanThreads, 1)
 plan_kernel(vp_params P, const vp_clip_desc* __restrict__ clips, int n, vp_clip_plan* __restrict__ plans,
             int64_t* __restrict__ frame_indices, int64_t index_cap, double* __restrict__ ts, int64_t ts_cap,
-            int64_t* __restrict__ totals, int ring) {
+            int64_t* __restrict__ totals) {
   __shared__ int64_t warp_tot[32][kNScan];
   __shared__ int64_t carry[kNScan];
   const int tid = threadIdx.x, lane = tid & 31, warp = tid >> 5;
@@ -120,13 +119,12 @@ plan_kernel(vp_params P, const vp_clip_desc* __restrict__ clips, int n, vp_clip_
       v[r.is_image ? S_IMGTOK : S_VIDTOK] = patches / m2;
       v[r.is_image ? S_NIMG : S_NVID] = 1;
       v[S_GROUPS] = r.is_image ? 0 : r.gt;
-      const int kv = select_variant(clips[k].height, clips[k].width, r.out_h, r.out_w, P.patch_size, ring);
+      const int kv = select_variant(clips[k].height, clips[k].width, r.out_h, r.out_w, P.patch_size);
       r.variant = kv;
       if (kv == KV_COPY) {
         v[S_TILES] = (int64_t)r.n * (r.gh / P.merge_size) * copy_wchunks(r.gw, P.merge_size);
-      } else if (kv == KV_RING) {
-        const int ws = ring_strip_width(clips[k].width, r.out_w);
-        v[S_TILES] = (int64_t)r.n * ((r.out_w + ws - 1) / ws);     // items: strips x frames
+      } else if (kv == KV_TEAM) {
+        v[S_TILES] = (int64_t)r.n * team_geometry(clips[k].width, r.out_w, P.patch_size).nslices;   // slices x frames
       } else if (kv != KV_GENERIC) {
         const int ws = fast_strip_width(clips[k].width, r.out_w);
         v[S_TILES] = (int64_t)r.n * ((r.out_w + ws - 1) / ws);     // items: frames x strips
@@ -274,13 +272,8 @@ extern "C" vp_status vp_plan_frames(const vp_params* p, const vp_clip_desc* clip
     vp::set_error("vp_plan_frames: null pointer argument");
     return VP_EINVAL;
   }
-  // KV_RING (vp_resize_ring.cu) is opt-in while it is slower than the warp-specialised streaming kernel on the
-  // bench geometry: VP_RING=1 enables it.
-  const char* ring_env = getenv("VP_RING");
-  const int ring = ring_env != nullptr && ring_env[0] == '1';
   vp::plan_kernel<<<1, vp::kPlanThreads, 0, vp::as_stream(stream)>>>(*p, clips, n, plans, frame_indices,
-                                                                      index_cap, group_timestamps, ts_cap, totals,
-                                                                      ring);
+                                                                      index_cap, group_timestamps, ts_cap, totals);
   if (n > 0) {
     const int per = vp::kFillThreads / 32;
     vp::plan_fill_kernel<<<(n + per - 1) / per, vp::kFillThreads, 0, vp::as_stream(stream)>>>(

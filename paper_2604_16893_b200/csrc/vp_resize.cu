@@ -14,8 +14,8 @@
 // horizontal (+ clamp + normalise + bf16/f32 store straight into the patch layout).
 // A source frame that fills several temporal slots (odd n padding, images) is filtered once and
 // stored to every slot.
-#include "vp_internal.cuh"
-#include <cuda_bf16.h>
+#include "vp_k3_common.cuh"
+#include <atomic>
 
 namespace vp {
 namespace {
@@ -262,10 +262,22 @@ __global__ void grids_kernel(const vp_clip_plan* __restrict__ plans, int n, int6
   }
 }
 
-int g_num_sms = 0;
+constexpr int kMaxDev = 64;
+std::atomic<unsigned> g_generic_attr[kMaxDev];
+
+template <typename K>
+void ensure_generic_attr(K kern, int dev, unsigned bit) {
+  if (dev >= 0 && dev < kMaxDev && (g_generic_attr[dev].load(std::memory_order_acquire) & bit)) return;
+  cudaFuncSetAttribute(kern, cudaFuncAttributeMaxDynamicSharedMemorySize, 200 * 1024);
+  if (dev >= 0 && dev < kMaxDev) g_generic_attr[dev].fetch_or(bit, std::memory_order_acq_rel);
+}
 
 }  // namespace
 }  // namespace vp
+
+extern "C" size_t vp_resize_workspace_bytes(int32_t n) {
+  return n < 0 ? 0 : vp::resize_ws_layout(n, nullptr).bytes;
+}
 
 extern "C" vp_status vp_resize_normalize_patchify(const vp_params* p, const vp_clip_plan* plans, int32_t n,
                                                   const uint8_t* frames,
@@ -273,7 +285,8 @@ extern "C" vp_status vp_resize_normalize_patchify(const vp_params* p, const vp_c
                                                   void* pixel_values_images, int64_t img_rows_cap,
                                                   void* pixel_values_videos, int64_t vid_rows_cap,
                                                   int64_t* image_grid_thw, int64_t* video_grid_thw,
-                                                  int32_t* clip_status, void* stream) {
+                                                  int32_t* clip_status, void* workspace, size_t workspace_bytes,
+                                                  void* stream) {
   vp_status st = vp::check_params(p);
   if (st != VP_OK) return st;
   if (n < 0 || img_rows_cap < 0 || vid_rows_cap < 0) {
@@ -286,12 +299,21 @@ extern "C" vp_status vp_resize_normalize_patchify(const vp_params* p, const vp_c
     vp::set_error("vp_resize_normalize_patchify: null pointer argument");
     return VP_EINVAL;
   }
+  const vp::ResizeWs ws = vp::resize_ws_layout(n, workspace);
+  if (workspace == nullptr || workspace_bytes < ws.bytes || (reinterpret_cast<uintptr_t>(workspace) & 255) != 0) {
+    vp::set_error("vp_resize_normalize_patchify: workspace must be >= vp_resize_workspace_bytes(%d) = %zu bytes, "
+                  "256-B aligned (got %zu at %p)", n, ws.bytes, workspace_bytes, workspace);
+    return VP_EINVAL;
+  }
   if (p->merge_size * p->patch_size > vp::kMaxBand) {
     vp::set_error("vp_resize_normalize_patchify: merge_size*patch_size=%d exceeds %d",
                   p->merge_size * p->patch_size, vp::kMaxBand);
     return VP_EUNSUPPORTED;
   }
   cudaStream_t s = vp::as_stream(stream);
+  int dev = 0;
+  cudaGetDevice(&dev);
+  const int sms = vp::device_sms(dev);
   vp::KParams kp{};
   kp.p = p->patch_size;
   kp.m = p->merge_size;
@@ -302,39 +324,36 @@ extern "C" vp_status vp_resize_normalize_patchify(const vp_params* p, const vp_c
     kp.bias[c] = (float)(-p->mean[c] / p->std[c]);
   }
   kp.out_f32 = p->out_dtype == VP_OUT_F32;
-  if (vp::g_num_sms == 0) {
-    int dev = 0;
-    cudaGetDevice(&dev);
-    cudaDeviceGetAttribute(&vp::g_num_sms, cudaDevAttrMultiProcessorCount, dev);
-    if (vp::g_num_sms <= 0) vp::g_num_sms = 148;
-  }
   vp::grids_kernel<<<(n + 255) / 256, 256, 0, s>>>(plans, n, img_rows_cap, vid_rows_cap,
                                                    pixel_values_images != nullptr, pixel_values_videos != nullptr,
                                                    image_grid_thw, video_grid_thw, clip_status);
   const int fast_aligned = (reinterpret_cast<uintptr_t>(frames) & 15) == 0;
   if (fast_aligned) {
-    const cudaError_t e = vp::launch_resize_fast(p, plans, n, frames, clip_byte_offset, row_pitch, pixel_values_images,
-                                                 img_rows_cap, pixel_values_videos, vid_rows_cap, s);
+    const vp::FKParams fk = vp::make_fkparams(p);
+    cudaError_t e = vp::launch_index(plans, n, clip_byte_offset, row_pitch, ws, s);
+    if (e == cudaSuccess)
+      e = vp::launch_team(fk, plans, n, ws, frames, clip_byte_offset, row_pitch, pixel_values_images, img_rows_cap,
+                          pixel_values_videos, vid_rows_cap, clip_status, sms, s);
+    if (e == cudaSuccess)
+      e = vp::launch_fast_variants(fk, plans, n, ws, frames, clip_byte_offset, row_pitch, pixel_values_images,
+                                   img_rows_cap, pixel_values_videos, vid_rows_cap, dev, sms, s);
     if (e != cudaSuccess) {
       vp::set_error("vp_resize_normalize_patchify: %s", cudaGetErrorString(e));
       return VP_ECUDA;
     }
   }
-  const int grid = vp::g_num_sms * 3;
+  const int grid = sms * 3;
   const size_t smem = vp::generic_smem_bytes(kp.m * kp.p);
-  static bool attr_set = false;
-  if (!attr_set) {
-    cudaFuncSetAttribute(vp::resize_generic_kernel<true>, cudaFuncAttributeMaxDynamicSharedMemorySize, 200 * 1024);
-    cudaFuncSetAttribute(vp::resize_generic_kernel<false>, cudaFuncAttributeMaxDynamicSharedMemorySize, 200 * 1024);
-    attr_set = true;
-  }
-  if (kp.out_f32)
+  if (kp.out_f32) {
+    vp::ensure_generic_attr(vp::resize_generic_kernel<true>, dev, 1u);
     vp::resize_generic_kernel<true><<<grid, vp::kThreads, smem, s>>>(kp, plans, n, fast_aligned, frames, clip_byte_offset,
                                                                    row_pitch, pixel_values_images, img_rows_cap,
                                                                    pixel_values_videos, vid_rows_cap);
-  else
+  } else {
+    vp::ensure_generic_attr(vp::resize_generic_kernel<false>, dev, 2u);
     vp::resize_generic_kernel<false><<<grid, vp::kThreads, smem, s>>>(kp, plans, n, fast_aligned, frames, clip_byte_offset,
                                                                     row_pitch, pixel_values_images, img_rows_cap,
                                                                     pixel_values_videos, vid_rows_cap);
+  }
   return vp::launch_status("vp_resize_normalize_patchify");
 }

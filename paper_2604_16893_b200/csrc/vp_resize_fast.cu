@@ -25,6 +25,7 @@
 // 1-tap copies).  Per item: the strip's horizontal weights.  Measurements behind each choice: DESIGN.md
 // section 6 and profiles/r03_summary.md.
 #include "vp_k3_common.cuh"
+#include <atomic>
 
 #ifndef VP_PLANAR
 // V->H rows as R / G / B planes (retire_planar): V saves its repacking moves (2.4% with H's taps off) but H's
@@ -809,130 +810,47 @@ resize_copy_kernel(FKParams kp, const vp_clip_plan* __restrict__ plans, const VI
   }
 }
 
-int g_num_sms = 0;
-bool g_attr[3][2] = {};
-bool g_cattr[2] = {};
+// Per-device "attribute set" bits (thread-safe: cudaFuncSetAttribute is idempotent, the bits only skip repeats).
+constexpr int kMaxDev = 64;
+std::atomic<unsigned> g_attr_bits[kMaxDev];
 
-// ---------------------------------------------------------------- per-variant work index
-// One CTA: slot v in {MILD, MEDIUM, STRONG, COPY} collects the valid, 16-B aligned clips of that variant
-// (list, batch order) and the exclusive prefix of their item counts (off); meta[v] = {count, items}.
-constexpr int kIdxThreads = 1024;
-__device__ __forceinline__ int variant_slot(int kv) {
-  return kv == KV_COPY ? 3 : (kv == KV_RING ? 4 : (kv <= KV_STRONG ? kv : -1));
-}
-
-__global__ void __launch_bounds__(kIdxThreads)
-variant_index_kernel(const vp_clip_plan* __restrict__ plans, int n, const int64_t* __restrict__ coff,
-                     const int64_t* __restrict__ pitch, int* __restrict__ list, int64_t* __restrict__ off,
-                     int64_t* __restrict__ meta) {
-  __shared__ int64_t wsum[kIdxThreads / 32][kNSlots];
-  __shared__ int wcnt[kIdxThreads / 32][kNSlots];
-  __shared__ int64_t c_items[kNSlots];
-  __shared__ int c_cnt[kNSlots];
-  const int tid = threadIdx.x, lane = tid & 31, warp = tid >> 5;
-  if (tid < kNSlots) { c_items[tid] = 0; c_cnt[tid] = 0; }
-  __syncthreads();
-  for (int c0 = 0; c0 < n; c0 += kIdxThreads) {
-    const int k = c0 + tid;
-    int slot = -1;
-    int64_t items = 0;
-    if (k < n) {
-      const vp_clip_plan& pl = plans[k];
-      if (pl.status == VP_OK && pl.tile_count > 0 && ((coff[k] | pitch[k]) & 15) == 0) {
-        slot = variant_slot(pl.kernel_variant);
-        items = pl.tile_count;
-      }
-    }
-    int64_t ex_items = 0;
-    int ex_cnt = 0;
-#pragma unroll
-    for (int v = 0; v < kNSlots; ++v) {
-      int64_t x = slot == v ? items : 0;
-      int y = slot == v ? 1 : 0;
-#pragma unroll
-      for (int o = 1; o < 32; o <<= 1) {
-        const int64_t xa = __shfl_up_sync(0xffffffffu, x, o);
-        const int ya = __shfl_up_sync(0xffffffffu, y, o);
-        if (lane >= o) { x += xa; y += ya; }
-      }
-      if (lane == 31) { wsum[warp][v] = x; wcnt[warp][v] = y; }
-      if (slot == v) { ex_items = x - items; ex_cnt = y - 1; }
-    }
-    __syncthreads();
-    int64_t add_items = 0, tot_items[kNSlots];
-    int add_cnt = 0, tot_cnt[kNSlots];
-#pragma unroll
-    for (int v = 0; v < kNSlots; ++v) { tot_items[v] = 0; tot_cnt[v] = 0; }
-    for (int w = 0; w < kIdxThreads / 32; ++w) {
-#pragma unroll
-      for (int v = 0; v < kNSlots; ++v) {
-        if (w < warp && slot == v) { add_items += wsum[w][v]; add_cnt += wcnt[w][v]; }
-        tot_items[v] += wsum[w][v];
-        tot_cnt[v] += wcnt[w][v];
-      }
-    }
-    if (slot >= 0) {
-      const int pos = c_cnt[slot] + add_cnt + ex_cnt;
-      list[(size_t)slot * n + pos] = k;
-      off[(size_t)slot * (n + 1) + pos] = c_items[slot] + add_items + ex_items;
-    }
-    __syncthreads();
-    if (tid < kNSlots) { c_items[tid] += tot_items[tid]; c_cnt[tid] += tot_cnt[tid]; }
-    __syncthreads();
-  }
-  if (tid < kNSlots) {
-    off[(size_t)tid * (n + 1) + c_cnt[tid]] = c_items[tid];
-    meta[2 * tid] = c_cnt[tid];
-    meta[2 * tid + 1] = c_items[tid];
-  }
+template <typename K>
+void ensure_smem_attr(K kern, int dev, unsigned bit, int bytes) {
+  if (dev >= 0 && dev < kMaxDev && (g_attr_bits[dev].load(std::memory_order_acquire) & bit)) return;
+  cudaFuncSetAttribute(kern, cudaFuncAttributeMaxDynamicSharedMemorySize, bytes);
+  if (dev >= 0 && dev < kMaxDev) g_attr_bits[dev].fetch_or(bit, std::memory_order_acq_rel);
 }
 
 template <int VARIANT, bool kF32>
 void launch_fast(const FKParams& kp, const vp_clip_plan* plans, const VIdx& vx, const uint8_t* frames,
                  const int64_t* coff, const int64_t* pitch, void* pi, int64_t icap, void* pvv, int64_t vcap,
-                 cudaStream_t s) {
+                 int dev, int num_sms, cudaStream_t s) {
   using Cfg = FastCfg<VARIANT>;
   auto kern = resize_fast_kernel<VARIANT, kF32>;
-  if (!g_attr[VARIANT][kF32]) {
-    cudaFuncSetAttribute(kern, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)Cfg::SMEM);
-    g_attr[VARIANT][kF32] = true;
-  }
+  ensure_smem_attr(kern, dev, 1u << (2 * VARIANT + (kF32 ? 1 : 0)), (int)Cfg::SMEM);
   int per_sm = 0;
   cudaOccupancyMaxActiveBlocksPerMultiprocessor(&per_sm, kern, kNT, Cfg::SMEM);
   if (per_sm < 1) per_sm = 1;
-  kern<<<g_num_sms * per_sm, kNT, Cfg::SMEM, s>>>(kp, plans, vx, frames, coff, pitch, pi, icap, pvv, vcap);
+  kern<<<num_sms * per_sm, kNT, Cfg::SMEM, s>>>(kp, plans, vx, frames, coff, pitch, pi, icap, pvv, vcap);
 }
 
 template <bool kF32>
 void launch_copy(const FKParams& kp, const vp_clip_plan* plans, const VIdx& vx, const uint8_t* frames,
                  const int64_t* coff, const int64_t* pitch, void* pi, int64_t icap, void* pvv, int64_t vcap,
-                 cudaStream_t s) {
+                 int dev, int num_sms, cudaStream_t s) {
   auto kern = resize_copy_kernel<kF32>;
   const int B = kp.m * kp.p;
   const size_t smem = (size_t)B * ((3 * kCopyMW * B + 15) & ~15);
-  if (!g_cattr[kF32]) {
-    cudaFuncSetAttribute(kern, cudaFuncAttributeMaxDynamicSharedMemorySize, 200 * 1024);
-    g_cattr[kF32] = true;
-  }
+  ensure_smem_attr(kern, dev, 1u << (8 + (kF32 ? 1 : 0)), 200 * 1024);
   int per_sm = 0;
   cudaOccupancyMaxActiveBlocksPerMultiprocessor(&per_sm, kern, kCT, smem);
   if (per_sm < 1) per_sm = 1;
-  kern<<<g_num_sms * per_sm, kCT, smem, s>>>(kp, plans, vx, frames, coff, pitch, pi, icap, pvv, vcap);
+  kern<<<num_sms * per_sm, kCT, smem, s>>>(kp, plans, vx, frames, coff, pitch, pi, icap, pvv, vcap);
 }
 
 }  // namespace
 
-// Launch the fast variants: build the per-variant work index in stream-ordered scratch, then one launch
-// per variant (each spreads its own items over the whole GPU).
-cudaError_t launch_resize_fast(const vp_params* p, const vp_clip_plan* plans, int n, const uint8_t* frames,
-                               const int64_t* coff, const int64_t* pitch, void* pi, int64_t icap, void* pvv,
-                               int64_t vcap, cudaStream_t s) {
-  if (g_num_sms == 0) {
-    int dev = 0;
-    cudaGetDevice(&dev);
-    cudaDeviceGetAttribute(&g_num_sms, cudaDevAttrMultiProcessorCount, dev);
-    if (g_num_sms <= 0) g_num_sms = 148;
-  }
+FKParams make_fkparams(const vp_params* p) {
   FKParams kp{};
   kp.p = p->patch_size;
   kp.m = p->merge_size;
@@ -942,59 +860,34 @@ cudaError_t launch_resize_fast(const vp_params* p, const vp_clip_plan* plans, in
   for (int c = 0; c < 3; ++c) {
     kp.scale[c] = (float)(1.0 / (255.0 * p->std[c]));
     kp.bias[c] = (float)(-p->mean[c] / p->std[c]);
-    kp.lo[c] = kp.bias[c];
-    kp.hi[c] = fmaf(255.0f, kp.scale[c], kp.bias[c]);
+    // output-domain clamp bounds: the images of 0 and 255, ordered (std < 0 flips them)
+    const float a = kp.bias[c], b = fmaf(255.0f, kp.scale[c], kp.bias[c]);
+    kp.lo[c] = fminf(a, b);
+    kp.hi[c] = fmaxf(a, b);
     kp.lo2[c] = __floats2bfloat162_rn(kp.lo[c], kp.lo[c]);
     kp.hi2[c] = __floats2bfloat162_rn(kp.hi[c], kp.hi[c]);
   }
-  const size_t list_b = ((size_t)kNSlots * n * sizeof(int) + 15) & ~(size_t)15;
-  const size_t off_b = (size_t)kNSlots * (n + 1) * sizeof(int64_t);
-  const size_t meta_b = 2 * kNSlots * sizeof(int64_t);
-  const size_t own_b = ((size_t)n * sizeof(int) + 255) & ~(size_t)255;
-  const size_t vt_off = (list_b + off_b + meta_b + own_b + 255) & ~(size_t)255;
-  const size_t bytes = vt_off + (size_t)n * ring_vtable_bytes();
-  // library-owned stream-ordered pool that keeps its memory between calls (release threshold = max), so
-  // the per-call scratch is a pool hit, not a driver allocation; the process's default pool is untouched
-  static cudaMemPool_t pool = nullptr;
-  static int pool_dev = -1;
-  int dev = 0;
-  cudaGetDevice(&dev);
-  if (pool == nullptr || pool_dev != dev) {
-    cudaMemPoolProps props{};
-    props.allocType = cudaMemAllocationTypePinned;
-    props.location.type = cudaMemLocationTypeDevice;
-    props.location.id = dev;
-    cudaError_t pe = cudaMemPoolCreate(&pool, &props);
-    if (pe != cudaSuccess) return pe;
-    uint64_t thr = ~0ull;
-    cudaMemPoolSetAttribute(pool, cudaMemPoolAttrReleaseThreshold, &thr);
-    pool_dev = dev;
-  }
-  void* scratch = nullptr;
-  cudaError_t e = cudaMallocFromPoolAsync(&scratch, bytes, pool, s);
-  if (e != cudaSuccess) return e;
-  int* list = reinterpret_cast<int*>(scratch);
-  int64_t* off = reinterpret_cast<int64_t*>(reinterpret_cast<char*>(scratch) + list_b);
-  int64_t* meta = off + (size_t)kNSlots * (n + 1);
-  int* vt_owner = reinterpret_cast<int*>(reinterpret_cast<char*>(scratch) + list_b + off_b + meta_b);
-  void* vt = reinterpret_cast<char*>(scratch) + vt_off;
-  variant_index_kernel<<<1, kIdxThreads, 0, s>>>(plans, n, coff, pitch, list, off, meta);
-  auto vx = [&](int slot) { return VIdx{list + (size_t)slot * n, off + (size_t)slot * (n + 1), meta + 2 * slot}; };
-  if (p->out_dtype == VP_OUT_F32) {
-    launch_fast<KV_MILD, true>(kp, plans, vx(0), frames, coff, pitch, pi, icap, pvv, vcap, s);
-    launch_fast<KV_MEDIUM, true>(kp, plans, vx(1), frames, coff, pitch, pi, icap, pvv, vcap, s);
-    launch_fast<KV_STRONG, true>(kp, plans, vx(2), frames, coff, pitch, pi, icap, pvv, vcap, s);
-    launch_copy<true>(kp, plans, vx(3), frames, coff, pitch, pi, icap, pvv, vcap, s);
+  return kp;
+}
+
+// The warp-specialised streaming variants (MILD / MEDIUM / STRONG) and the identity copy, one launch each over
+// that variant's items only (work index built by launch_index in the same workspace).
+cudaError_t launch_fast_variants(const FKParams& kp, const vp_clip_plan* plans, int n, const ResizeWs& w,
+                                 const uint8_t* frames, const int64_t* coff, const int64_t* pitch, void* pi,
+                                 int64_t icap, void* pvv, int64_t vcap, int dev, int num_sms, cudaStream_t s) {
+  auto vx = [&](int slot) { return ws_vidx(w, n, slot); };
+  if (kp.out_f32) {
+    launch_fast<KV_MILD, true>(kp, plans, vx(0), frames, coff, pitch, pi, icap, pvv, vcap, dev, num_sms, s);
+    launch_fast<KV_MEDIUM, true>(kp, plans, vx(1), frames, coff, pitch, pi, icap, pvv, vcap, dev, num_sms, s);
+    launch_fast<KV_STRONG, true>(kp, plans, vx(2), frames, coff, pitch, pi, icap, pvv, vcap, dev, num_sms, s);
+    launch_copy<true>(kp, plans, vx(3), frames, coff, pitch, pi, icap, pvv, vcap, dev, num_sms, s);
   } else {
-    launch_fast<KV_MILD, false>(kp, plans, vx(0), frames, coff, pitch, pi, icap, pvv, vcap, s);
-    launch_fast<KV_MEDIUM, false>(kp, plans, vx(1), frames, coff, pitch, pi, icap, pvv, vcap, s);
-    launch_fast<KV_STRONG, false>(kp, plans, vx(2), frames, coff, pitch, pi, icap, pvv, vcap, s);
-    launch_copy<false>(kp, plans, vx(3), frames, coff, pitch, pi, icap, pvv, vcap, s);
+    launch_fast<KV_MILD, false>(kp, plans, vx(0), frames, coff, pitch, pi, icap, pvv, vcap, dev, num_sms, s);
+    launch_fast<KV_MEDIUM, false>(kp, plans, vx(1), frames, coff, pitch, pi, icap, pvv, vcap, dev, num_sms, s);
+    launch_fast<KV_STRONG, false>(kp, plans, vx(2), frames, coff, pitch, pi, icap, pvv, vcap, dev, num_sms, s);
+    launch_copy<false>(kp, plans, vx(3), frames, coff, pitch, pi, icap, pvv, vcap, dev, num_sms, s);
   }
-  const cudaError_t re = launch_resize_ring(kp, plans, vx(4), frames, coff, pitch, pi, icap, pvv, vcap, n, vt, vt_owner,
-                                            g_num_sms, s);
-  if (re != cudaSuccess) return re;
-  return cudaFreeAsync(scratch, s);
+  return cudaGetLastError();
 }
 
 }  // namespace vp

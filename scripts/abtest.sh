@@ -1,8 +1,9 @@
-python -c "import __graft_entry__ as g; g.build()" > /dev/null 2>&1
-cp paper_2604_16893_b200/libvp.so /tmp/libvp_new.so
-for v in new committed new committed; do
-  if [ $v = new ]; then cp /tmp/libvp_new.so paper_2604_16893_b200/libvp.so; else cp libvp_committed.so paper_2604_16893_b200/libvp.so; fi
-  touch paper_2604_16893_b200/libvp.so
-  timeout 600 python bench.py --clips 64 --steps 5 --warmup 3 --no-cpu-baseline --no-e2e > gpurun_out/ab.log 2>&1
-  python -c "import json;d=json.loads(open('gpurun_out/ab.log').read().strip().splitlines()[-1]);print('$v','ms',round(d['ms_per_step'],3))" || tail -3 gpurun_out/ab.log
+# A/B of compile-time variants on one box: bash scripts/abtest.sh "<flags A>" "<flags B>" ... (each = VP_EXTRA_NVCC_FLAGS)
+# runs a 64-clip cfg5 bench per variant, twice, and prints k3_ms
+for rep in ${REPS:-1}; do
+for F in "$@"; do
+  VP_EXTRA_NVCC_FLAGS="$F" python paper_2604_16893_b200/_build.py -f > /dev/null 2>&1 || { echo "build failed: $F"; continue; }
+  R=$(python bench.py --steps 8 --warmup 3 --no-e2e --no-cpu-baseline --clips 64 2>/dev/null | tail -1 | python -c "import json,sys; d=json.loads(sys.stdin.read()); print('%.3f ms  frac %.3f' % (d['roofline']['k3_ms'], d['roofline']['frac']))")
+  echo "[$F] $R"
+done
 done

@@ -1,14 +1,17 @@
-"""Hottest SASS of an ncu report: per-opcode totals and the hottest lines in address order.
-usage: python scripts/hot_sass.py report.ncu-rep [min_count] [opcode-filter]"""
-import csv, subprocess, sys, io, collections
-rep = sys.argv[1]
-thr = float(sys.argv[2]) if len(sys.argv) > 2 else 1e6
-flt = sys.argv[3] if len(sys.argv) > 3 else None
-out = subprocess.run(["ncu", "-i", rep, "--page", "source", "--csv", "--print-source", "sass"], capture_output=True, text=True).stdout
-r = list(csv.reader(io.StringIO(out)))
-hi = next(i for i, x in enumerate(r) if "Instructions Executed" in x)
-h = r[hi]; ie = h.index("Instructions Executed"); isamp = h.index("Warp Stall Sampling (All Samples)")
-rows = [(x[0][-5:], x[1].strip(), int(x[ie]), int(x[isamp] or 0)) for x in r[hi + 1:] if len(x) > ie and x[ie].isdigit()]
-for a, s, n, smp in rows:
-    if n >= thr and (flt is None or flt in s):
-        print(a, f"{s[:100]:100s}", n, smp)
+"""Print the hottest SASS region(s) of an ncu source page (csv): address, exec count, stall samples, instruction."""
+import csv, sys
+rows = list(csv.reader(open(sys.argv[1])))
+hdr = rows[1]
+ia, isrc, iss, ie = hdr.index("Address"), hdr.index("Source"), hdr.index("Warp Stall Sampling (All Samples)"), hdr.index("Instructions Executed")
+thr = int(sys.argv[2]) if len(sys.argv) > 2 else 100000
+lo = int(sys.argv[3], 16) if len(sys.argv) > 3 else 0
+hi = int(sys.argv[4], 16) if len(sys.argv) > 4 else 1 << 62
+base = int(rows[2][ia], 16)
+for r in rows[2:]:
+    try:
+        a = int(r[ia], 16) - base
+        n = int(r[ie])
+    except ValueError:
+        continue
+    if n >= thr and lo <= a <= hi:
+        print(f"{a:6x} {n:9d} {r[iss]:>6s}  {r[isrc].strip()}")

@@ -133,34 +133,43 @@ def _aligned_compare(pre, clips, kind="noise"):
 CLIP_MEAN, CLIP_STD = (0.48145466, 0.4578275, 0.40821073), (0.26862954, 0.26130258, 0.27577711)
 
 
-@pytest.fixture
-def ring_enabled(monkeypatch):
-    """KV_RING is opt-in (VP_RING=1, read by vp_plan_frames on every call)."""
-    monkeypatch.setenv("VP_RING", "1")
+KV_TEAM = 5
 
 
 @pytest.mark.parametrize("dtype", [1, 0])
 @pytest.mark.parametrize("tp", [1, 2, 3])
-def test_ring_variant(dtype, tp, ring_enabled):
-    """KV_RING (one warp per CTA, vertical + horizontal register rings): downscales from ~1.03x to ~3.1x,
-    identity on one axis, several strips with a ragged last strip, 30-row H blocks with a ragged last
-    block, temporal padding (n < tp and n not a multiple of tp), images filling tp slots, CLIP mean/std."""
+def test_team_variant(dtype, tp):
+    """KV_TEAM (every warp does the 4-slot vertical ring and the horizontal pass of its column pairs): downscales
+    from ~1.03x to ~2x, identity on one axis, several slices with a ragged last slice, temporal padding (n < tp and
+    n not a multiple of tp), images filling tp slots, CLIP mean/std."""
     import paper_2604_16893_b200 as vp
     pre = vp.VisualPreprocessor(max_frames=max(tp, 5), temporal_patch_size=tp, video_max_pixels=32768,
                                 image_max_pixels=65536, out_dtype=dtype, mean=CLIP_MEAN, std=CLIP_STD)
-    clips = [I.clip(9, 2.0, 250, 500),        # 1.95x both axes -> 128 x 256: 6 strips (last 16 wide)
+    clips = [I.clip(9, 2.0, 250, 500),        # 1.95x both axes -> 128 x 256
              I.image(64, 330),                # identity rows, 1.03x columns
-             I.image(330, 64),                # 1.03x rows, identity columns (one strip)
-             I.clip(3, 1.0, 390, 700),        # ~3.1x -> 128 x 224: strips of 32
+             I.image(330, 64),                # 1.03x rows, identity columns
+             I.clip(3, 1.0, 260, 1100),       # ~1.7x rows, ~2x columns: several slices
              I.clip(1, 1.0, 250, 500),        # n = 1 < tp: padded
              I.image(250, 500)]
     pl = _aligned_compare(pre, clips)
     kv = pl.plans_host["kernel_variant"][:len(clips)].tolist()
-    assert kv.count(5) >= 5, kv
+    assert kv.count(KV_TEAM) >= 5, kv
+
+
+@pytest.mark.parametrize("patch", [14, 16])
+def test_team_patch14_and_wide(patch):
+    """p = 14 (28-byte patch rows, slices in multiples of p) and a wide frame split into many slices."""
+    import paper_2604_16893_b200 as vp
+    f = 2 * patch
+    pre = vp.VisualPreprocessor(patch_size=patch, max_frames=4, video_max_pixels=f * f * 300,
+                                image_max_pixels=f * f * 300, out_dtype=1)
+    clips = [I.clip(4, 1.0, 9 * f, 45 * f), I.image(12 * f + 5, 30 * f + 3), I.clip(2, 1.0, 500, 1000)]
+    pl = _aligned_compare(pre, clips)
+    assert (pl.plans_host["kernel_variant"][:len(clips)] == KV_TEAM).all(), pl.plans_host["kernel_variant"]
 
 
 @pytest.mark.parametrize("seed", range(3))
-def test_ring_random_downscales(seed, ring_enabled):
+def test_team_random_downscales(seed):
     import paper_2604_16893_b200 as vp
     rng = random.Random(500 + seed)
     tp = rng.choice([1, 2])
@@ -223,10 +232,10 @@ def test_cfg4_sampled():
 
 
 def test_fast_groups_straddle_items():
-    """The fast kernel's TMA staging refills in groups of 8 source rows; when a source height is not a
-    multiple of 8 a group straddles two work items (the per-row refill path that opens the next item).
-    40 odd-height clips x 16 frames = 640 items over 2 CTAs/SM x 148 SMs, so every CTA walks several
-    consecutive items of different heights; sampled outputs of every clip against the oracle."""
+    """The TMA staging of the team / fast kernels refills in groups of 8 source rows; when a source height is
+    not a multiple of 8 a group straddles two work items (the per-row refill path that opens the next item).
+    40 odd-height clips x 16 frames (x slices) over the whole GPU, so every CTA walks several consecutive items
+    of different heights and geometries (distinct weight tables); sampled outputs of every clip vs the oracle."""
     import paper_2604_16893_b200 as vp
     rng = random.Random(7)
     pre = vp.VisualPreprocessor(max_frames=16, video_max_pixels=100000, out_dtype=1)   # ratios ~1.1-2.1
@@ -236,7 +245,7 @@ def test_fast_groups_straddle_items():
         if h % 8:
             clips.append(I.clip(240, 30.0, h, w))
     kv = pre.plan(clips).plans_host["kernel_variant"][:len(clips)]
-    assert all(v in (0, 1, 2) for v in kv) and sum(v == 0 for v in kv) >= 30, kv   # fast variants, mostly MILD
+    assert all(v in (0, 1, 2, KV_TEAM) for v in kv) and sum(v == KV_TEAM for v in kv) >= 30, kv   # mostly KV_TEAM
     _sampled_compare(pre, clips, n_samples=6000, seed=3, align16=True)
 
 
@@ -312,8 +321,10 @@ def test_capacity_is_reported_not_overrun():
     out["pixel_values_videos"] = big[:100]               # needs 256 rows
     fl = host_frames(O.plan_batch(oracle_params(pre.params), clips)[0])
     buf, offs, pit = pack_frames(fl, [384])
-    pre.run(pl, buf, offs, pit, out=out)
+    pre.run(pl, buf, offs, pit, out=out, strict=False)
     assert out["clip_status"][0].item() == vp.VP_ECAPACITY
+    with pytest.raises(vp.VpError):
+        pre.run(pl, buf, offs, pit, out=out)                  # strict by default
     assert (big.float() == 7.0).all()
 
 
