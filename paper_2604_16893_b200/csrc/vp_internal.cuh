@@ -50,7 +50,7 @@ constexpr int kTotLen = VP_TOT_LEN;
 // KV_GENERIC covers everything else (vp_resize.cu, token tiles).  A clip's items (tile_count)
 // are n_frames x n_strips for the fast variants, 0 for generic.  Integer / f64 exact.
 // ------------------------------------------------------------------------------------------
-enum { KV_MILD = 0, KV_MEDIUM = 1, KV_STRONG = 2, KV_GENERIC = 3, KV_COPY = 4, KV_TEAM = 5 };
+enum { KV_MILD = 0, KV_MEDIUM = 1, KV_STRONG = 2, KV_GENERIC = 3, KV_COPY = 4, KV_TEAM = 5, KV_WIDE = 6 };
 constexpr int kRing = 5;          // vertical ring slots: max live output rows per source row for in/out > 0.8
 constexpr int kInHMax = 1088;     // source rows supported by the fast kernel's per-row weight table
 constexpr int kWListMax = 6144;   // vertical weights (sum of window lengths) held in smem
@@ -97,14 +97,18 @@ __host__ __device__ __forceinline__ int fast_strip_width(int in_w, int out_w) {
 constexpr int kCopyMW = 8;
 __host__ __device__ __forceinline__ int copy_wchunks(int grid_w, int m) { return (grid_w / m + kCopyMW - 1) / kCopyMW; }
 
-// KV_TEAM (vp_resize_team.cu): a CTA of kTeamW warps walks one (clip, slice, frame) item; every warp does the
-// vertical ring on a 128-pixel part of the slice footprint and the horizontal pass of its column pairs.  Needs a
-// downscale or identity on both axes (then <= 4 output rows are live per source row), an even
-// patch size (bf16x2 / float2 column pairs), a horizontal union window (column pair) of <= kTeamUL taps and the
-// per-clip tables (kTabInH source rows, kTabOutH output rows).  Slices are multiples of p columns (each patch row
-// is written by one CTA: no partially written sectors shared between CTAs) of <= 64*kTeamW columns whose footprint
-// fits 128*kTeamW pixels; the slice count is balanced.  Items per clip: n_frames x nslices.
-constexpr int kTeamW = 4;         // warps per team CTA
+// KV_TEAM / KV_WIDE (vp_resize_team.cu): a CTA of NV "V" warps and NH "H" warps walks one (clip, slice, frame)
+// item; each V warp runs the 4-slot vertical ring on a 128-pixel part of the slice footprint and retires finished
+// output rows into shared memory; each H warp does the horizontal pass of 32 column pairs.  Needs a downscale or
+// identity on both axes (then <= 4 output rows are live per source row), an even patch size
+// (bf16x2 / float2 column pairs), a horizontal union window (column pair) of <= kTeamUL taps and the per-clip
+// tables (kTabInH source rows, kTabOutH output rows).  KV_WIDE (NV = 10, NH = 11) takes whole frames up to 1280
+// pixels wide in one slice (no halo: every V lane does unique work); KV_TEAM (NV = NH = 4) cuts wider / other
+// frames into slices of multiples of p columns (each patch row is written by one CTA: no partially written
+// sectors shared between CTAs) of <= 64*NH columns whose footprint fits 128*NV pixels, balanced in width.
+// Items per clip: n_frames x nslices.
+constexpr int kTeamNV = 4, kTeamNH = 4, kTeamPPL = 1;    // V warps, H warps, column pairs per H lane
+constexpr int kWideNV = 10, kWideNH = 6, kWidePPL = 2;
 constexpr int kTeamUL = 10;       // union taps of a column pair (registers)
 constexpr int kTabInH = 1088;     // per-clip vertical weight records (float4 per source row)
 constexpr int kTabOutH = 1088;    // per-clip window ends (int per output row, padded to a multiple of 4)
@@ -112,15 +116,20 @@ constexpr int kTabOutH = 1088;    // per-clip window ends (int per output row, p
 struct TeamGeo {
   int ws, nslices;                // slice width (columns), slices per frame; ws = 0: does not fit
 };
-__host__ __device__ __forceinline__ TeamGeo team_geometry(int in_w, int out_w, int p) {
+__host__ __device__ __forceinline__ TeamGeo team_geometry(int in_w, int out_w, int p, int nv, int nh) {
   TeamGeo g{0, 0};
   if (p < 2 || (p & 1) || out_w < p) return g;
+  if (in_w <= 128 * nv && out_w <= 64 * nh) {     // one slice: the footprint is the whole row [0, in_w)
+    g.ws = out_w;
+    g.nslices = 1;
+    return g;
+  }
   const double s = (double)in_w / (double)out_w;
   const double fs = s > 1.0 ? s : 1.0;
   // footprint of c consecutive columns from a 4-pixel aligned start: < (c-1)*s + 4*fs + 1 + 3 pixels
   int cmax = 0;
-  for (int c = p; c <= 64 * kTeamW && c <= out_w; c += p)
-    if ((c - 1) * s + 4.0 * fs + 4.0 + 0.01 <= 128.0 * kTeamW) cmax = c;
+  for (int c = p; c <= 64 * nh && c <= out_w; c += p)
+    if ((c - 1) * s + 4.0 * fs + 4.0 + 0.01 <= 128.0 * nv) cmax = c;
   if (cmax == 0) return g;
   const int n = (out_w + cmax - 1) / cmax;
   int ws = (out_w + n - 1) / n;
@@ -130,6 +139,8 @@ __host__ __device__ __forceinline__ TeamGeo team_geometry(int in_w, int out_w, i
   g.nslices = (out_w + ws - 1) / ws;
   return g;
 }
+__host__ __device__ __forceinline__ int variant_nv(int kv) { return kv == KV_WIDE ? kWideNV : kTeamNV; }
+__host__ __device__ __forceinline__ int variant_nh(int kv) { return kv == KV_WIDE ? kWideNH * kWidePPL : kTeamNH * kTeamPPL; }
 // taps of the union of two adjacent columns' windows: x1(j+1) - x0(j) < s + 4*fs + 1
 __host__ __device__ __forceinline__ int pair_union_bound(int in, int out) {
   const double s = (double)in / (double)out;
@@ -140,8 +151,11 @@ __host__ __device__ __forceinline__ int pair_union_bound(int in, int out) {
 __host__ __device__ __forceinline__ int select_variant(int in_h, int in_w, int out_h, int out_w, int p) {
   if (in_h == out_h && in_w == out_w && (p & 1) == 0) return KV_COPY;
   if (in_h >= out_h && in_w >= out_w && (p & 1) == 0 && in_h <= kTabInH && out_h <= kTabOutH &&
-      pair_union_bound(in_w, out_w) <= kTeamUL && team_geometry(in_w, out_w, p).ws > 0)
-    return KV_TEAM;
+      pair_union_bound(in_w, out_w) <= kTeamUL) {
+    if (in_w <= 128 * kWideNV && out_w <= 64 * kWideNH * kWidePPL && team_geometry(in_w, out_w, p, kWideNV, variant_nh(KV_WIDE)).ws > 0)
+      return KV_WIDE;
+    if (team_geometry(in_w, out_w, p, kTeamNV, variant_nh(KV_TEAM)).ws > 0) return KV_TEAM;
+  }
   const double sv = (double)in_h / (double)out_h;
   // live output rows per source row <= floor(4/s)+1 for upscale (<= 5 iff s > 0.8) and <= 5 for downscale
   // (trimmed windows; brute-forced in tests/test_oracle_pixels.py::test_live_rows_bound).  The streaming kernel

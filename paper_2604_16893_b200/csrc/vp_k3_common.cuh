@@ -54,6 +54,31 @@ __device__ __forceinline__ void mbar_wait(uint64_t* bar, uint32_t parity) {
       "r"(parity)
       : "memory");
 }
+// Warp-uniform wait (every lane tests the same barrier phase in one instruction, so the retry branch is uniform:
+// bra.uni spares ptxas the divergence bookkeeping around the loop).  kHint > 0 adds a suspend-time hint (ns).
+template <int kHint = 0>
+__device__ __forceinline__ void mbar_wait_uni(uint64_t* bar, uint32_t parity) {
+  if (kHint > 0)
+    asm volatile(
+        "{\n"
+        ".reg .pred P1;\n"
+        "WAITH_%=:\n"
+        "mbarrier.try_wait.parity.acquire.cta.shared::cta.b64 P1, [%0], %1, %2;\n"
+        "@!P1 bra.uni WAITH_%=;\n"
+        "}\n" ::"r"(smem_u32(bar)),
+        "r"(parity), "n"(kHint)
+        : "memory");
+  else
+    asm volatile(
+        "{\n"
+        ".reg .pred P1;\n"
+        "WAITU_%=:\n"
+        "mbarrier.try_wait.parity.acquire.cta.shared::cta.b64 P1, [%0], %1;\n"
+        "@!P1 bra.uni WAITU_%=;\n"
+        "}\n" ::"r"(smem_u32(bar)),
+        "r"(parity)
+        : "memory");
+}
 // Wait with a suspend-time hint: the thread may be suspended (not re-issuing try_wait) until the phase
 // completes or the hint expires -- for consumers that routinely wait long (H warps waiting on V rows), so that
 // spinning does not take issue slots from the warps doing the work.
@@ -150,8 +175,8 @@ __device__ __forceinline__ int vfind(const VIdx& vx, int cnt, int64_t item) {   
   return lo;
 }
 
-// Per-variant work-index slots (variant_index_kernel): MILD, MEDIUM, STRONG, COPY, TEAM.
-constexpr int kNSlots = 5;
+// Per-variant work-index slots (variant_index_kernel): MILD, MEDIUM, STRONG, COPY, TEAM, WIDE.
+constexpr int kNSlots = 6;
 
 // Caller workspace of vp_resize_normalize_patchify (resize_ws_layout): the per-variant work index and the
 // KV_TEAM per-clip tables.  Nothing persists between calls.
@@ -160,7 +185,7 @@ struct ResizeWs {
   int* list;          // [kNSlots][n]
   int64_t* off;       // [kNSlots][n+1]
   int64_t* meta;      // [kNSlots][2]
-  int* alias;         // [n]  TEAM list position -> table owner
+  int* alias;         // [n]  clip -> first clip of its run of equal (in_h, out_h) TEAM / WIDE clips (table owner)
   int* tflag;         // [n]  table flags (a non-negligible 5th live row)
   float4* vtab;       // [n][kTabInH]
   int* y1tab;         // [n][kTabOutH]
@@ -172,7 +197,7 @@ cudaError_t launch_index(const vp_clip_plan* plans, int n, const int64_t* coff, 
                          const ResizeWs& w, cudaStream_t s);
 cudaError_t launch_team(const FKParams& kp, const vp_clip_plan* plans, int n, const ResizeWs& w, const uint8_t* frames,
                         const int64_t* coff, const int64_t* pitch, void* pi, int64_t icap, void* pvv, int64_t vcap,
-                        int32_t* clip_status, int num_sms, cudaStream_t s);
+                        int32_t* clip_status, int dev, int num_sms, cudaStream_t s);
 cudaError_t launch_fast_variants(const FKParams& kp, const vp_clip_plan* plans, int n, const ResizeWs& w,
                                  const uint8_t* frames, const int64_t* coff, const int64_t* pitch, void* pi,
                                  int64_t icap, void* pvv, int64_t vcap, int dev, int num_sms, cudaStream_t s);

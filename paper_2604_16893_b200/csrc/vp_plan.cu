@@ -123,8 +123,9 @@ plan_kernel(vp_params P, const vp_clip_desc* __restrict__ clips, int n, vp_clip_
       r.variant = kv;
       if (kv == KV_COPY) {
         v[S_TILES] = (int64_t)r.n * (r.gh / P.merge_size) * copy_wchunks(r.gw, P.merge_size);
-      } else if (kv == KV_TEAM) {
-        v[S_TILES] = (int64_t)r.n * team_geometry(clips[k].width, r.out_w, P.patch_size).nslices;   // slices x frames
+      } else if (kv == KV_TEAM || kv == KV_WIDE) {
+        v[S_TILES] = (int64_t)r.n *
+                     team_geometry(clips[k].width, r.out_w, P.patch_size, variant_nv(kv), variant_nh(kv)).nslices;
       } else if (kv != KV_GENERIC) {
         const int ws = fast_strip_width(clips[k].width, r.out_w);
         v[S_TILES] = (int64_t)r.n * ((r.out_w + ws - 1) / ws);     // items: frames x strips

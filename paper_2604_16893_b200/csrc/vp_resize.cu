@@ -333,7 +333,7 @@ extern "C" vp_status vp_resize_normalize_patchify(const vp_params* p, const vp_c
     cudaError_t e = vp::launch_index(plans, n, clip_byte_offset, row_pitch, ws, s);
     if (e == cudaSuccess)
       e = vp::launch_team(fk, plans, n, ws, frames, clip_byte_offset, row_pitch, pixel_values_images, img_rows_cap,
-                          pixel_values_videos, vid_rows_cap, clip_status, sms, s);
+                          pixel_values_videos, vid_rows_cap, clip_status, dev, sms, s);
     if (e == cudaSuccess)
       e = vp::launch_fast_variants(fk, plans, n, ws, frames, clip_byte_offset, row_pitch, pixel_values_images,
                                    img_rows_cap, pixel_values_videos, vid_rows_cap, dev, sms, s);

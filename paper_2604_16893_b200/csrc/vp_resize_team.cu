@@ -1,25 +1,26 @@
-// vp_resize_team.cu -- K3 "team" kernel: streaming fused AA-bicubic resize + clamp + normalise + temporal pad +
-// patchify (O4-O9) for downscales / identity on both axes with a narrow horizontal window (KV_TEAM).
+// vp_resize_team.cu -- K3 team kernels (KV_TEAM, KV_WIDE): streaming fused AA-bicubic resize + clamp + normalise +
+// temporal pad + patchify (O4-O9) for downscales / identity on both axes with a narrow horizontal window.
 //
-// Work item = (clip, slice, source frame f): a slice is a 16-column-aligned range of <= 64*kTeamW output columns
-// whose source footprint fits kTeamW*128 pixels.  A CTA ("team") of kTeamW warps walks the item's source rows top
-// to bottom exactly once.  Every warp does both passes (no producer/consumer warp specialisation):
-//   V: the warp owns a 128-pixel (384-byte) part of the footprint; lane L converts its 12 bytes (4 RGB pixels) of
+// Work item = (clip, slice, source frame f).  A slice is a range of output columns whose source footprint fits the
+// CTA's NV*128 pixels (KV_WIDE: the whole frame row).  A CTA of NV V warps + NH H warps walks the item's source rows
+// top to bottom exactly once:
+//   V warps: warp v owns a 128-pixel (384-byte) part of the footprint; lane L converts its 12 bytes (4 RGB pixels) of
 //      each staged source row once (I2F.U8 on the XU pipe for 2 of 3 words, PRMT + FADD2 for the third: both exact)
 //      and FMAs them (FFMA2, broadcast weight) into a 4-slot register ring of live output rows.  For a downscale
 //      (in >= out) at most 4 output rows are live at any source row (window 4s wide, centres s apart),
 //      so 4 slots carry no dead FMAs at the bench ratio.  Output row i lives in slot i % 4; the output-row loop is
-//      unrolled by 4 so every slot index -- and the parity of i, which picks the retire buffer -- is static.
-//   retire: when output row i is complete, each lane stores its 4 pixels (float4 RGB + pad) into retire buffer
-//      i & 1 (sub-pixel-major swizzle: conflict-free stores, ~1.3x wavefronts for the H taps), then ONE CTA barrier.
-//   H: lane (warp w, lane l) owns output column pair q = 32w + l of the slice; the pair's union window (<= kUL taps,
-//      weights (w_a, w_b) and swizzled tap offsets held in registers for the whole slice) is read once per row
-//      (LDS.128) and FMA'd as 3 FFMA2 (pixel channel broadcast x pair weights); normalise (FFMA2), clamp in the
-//      output domain, pack bf16x2 / float2 and store straight into the HF patch layout, once per temporal slot.
-// Double-buffered retire rows + one barrier per output row are race-free: a warp writes buffer i&1 again only
-// after passing barrier i+1, which every warp reaches after finishing its H of row i.
+//      unrolled by 4 so every slot index is static.  A finished row is stored (float4 RGB + pad per pixel,
+//      sub-pixel-major swizzle: conflict-free stores, ~1.3x wavefronts for the H taps) into one of kNR retire
+//      slots: wait until the H warps released the slot (mbarrier rempty), store, arrive on rfull.
+//   H warps: lane (warp h, lane l) owns output column pair q = 32h + l of the slice; the pair's union window
+//      (<= kUL taps; weights (w_a, w_b) and the taps' shared addresses in registers for the whole slice) is read once
+//      per row (LDS.128) and FMA'd as 3 FFMA2 (pixel channel broadcast x pair weights); normalise (FFMA2), clamp in
+//      the output domain, pack bf16x2 / float2 and store straight into the HF patch layout, once per temporal slot
+//      the frame fills (O7); then release the retire slot.
+// The roles keep their own registers (V: the 48-register ring; H: 30 registers of slice state), so a CTA of 21
+// warps fits one SM with no spills, and V runs up to kNR rows ahead of H.
 //
-// Staging: each warp keeps kTDepth source rows of its part in flight with cp.async.bulk (refilled in groups of
+// Staging: each V warp keeps kTDepth source rows of its part in flight with cp.async.bulk (refilled in groups of
 // kTGrp rows, one mbarrier per group, producer state warp-uniform with the copies predicated to lane 0).  The
 // vertical weights travel with the rows: per source row a 16-B record (the fp32 weights of its <= 4 live output
 // rows, relative to the row being completed) copied by TMA from the per-clip table that team_vtab_kernel writes
@@ -31,61 +32,69 @@
 namespace vp {
 namespace {
 
-constexpr int kTW = kTeamW;                 // warps per CTA (team)
-constexpr int kTT = kTW * 32;               // threads per CTA
 #ifndef VP_TEAM_DEPTH
 #define VP_TEAM_DEPTH 16
 #endif
-#ifndef VP_TEAM_PF
-#define VP_TEAM_PF 0        // software-prefetch the next staged row (bytes + weight record) one row ahead
-#endif
-constexpr int kTDepth = VP_TEAM_DEPTH;      // staged source rows per warp
+constexpr int kTDepth = VP_TEAM_DEPTH;      // staged source rows per V warp
 constexpr int kTGrp = 8;                    // rows per refill group (one mbarrier phase)
 constexpr int kTNGrp = kTDepth / kTGrp;
 constexpr int kTRowB = 400;                 // staged bytes per row slot: 384 + 16-B alignment slack
-constexpr int kTPx = kTW * 128;             // footprint pixels per team (power of two)
-static_assert((kTPx & (kTPx - 1)) == 0, "retire row index wraps with a mask");
+#ifndef VP_TEAM_NR
+#define VP_TEAM_NR 4
+#endif
+constexpr int kNR = VP_TEAM_NR;             // retire slots (rows V may run ahead of H)
+#ifndef VP_TEAM_HINT
+#define VP_TEAM_HINT 0      // suspend-time hint (ns) of the V<->H retire-slot waits; 0 = spin
+#endif
 
-struct TeamSmem {
-  uint8_t stage[kTW][kTDepth][kTRowB];      // source rows
-  float4 wrec[kTW][kTDepth];                // their vertical weight records
-  float4 buf[2][kTPx];                      // retired output rows (swizzled pixel-major RGB + pad)
-  uint64_t full[kTW][kTNGrp];               // staging groups: TMA -> warp
-  int4 prod[kTW][3];                        // per-warp producer state (TeamProd)
+template <int NV, int NH>
+struct SplitCfg {
+  static constexpr int kPx = NV * 128;                                    // footprint pixels per CTA
+  static constexpr int kThreads = (NV + NH) * 32;
+  static constexpr int kRowB = (NV * 384 + 16 + 15) & ~15;                // staged row: footprint + alignment slack
+  static constexpr size_t OFF_STG = 0;
+  static constexpr size_t OFF_WREC = OFF_STG + (size_t)kTDepth * kRowB;
+  static constexpr size_t OFF_BUF = OFF_WREC + (size_t)kTDepth * 16;
+  static constexpr size_t OFF_SBAR = OFF_BUF + (size_t)kNR * kPx * 16;
+  static constexpr size_t OFF_RBAR = OFF_SBAR + (size_t)kTNGrp * 8;
+  static constexpr size_t OFF_CNT = OFF_RBAR + (size_t)2 * kNR * 8;
+  static constexpr size_t OFF_PROD = (OFF_CNT + (size_t)kTNGrp * 4 + 15) & ~(size_t)15;
+  static constexpr size_t SMEM = OFF_PROD + 48;
+  static_assert(OFF_WREC % 16 == 0 && OFF_BUF % 16 == 0 && OFF_SBAR % 8 == 0 && OFF_PROD % 16 == 0, "align");
 };
 
-// Per-warp producer state (warp-uniform; kept in shared memory between refills so that it does not occupy
-// registers in the row loop).
+// Producer state of the CTA's staging ring (shared memory; read and updated only by the V warp that refills a
+// group -- refills are serialised because the last reader of group g+1 starts after the refill of g was issued).
 struct TeamProd {
-  const uint8_t* src;       // next source row of this warp's part (16-B aligned)
+  const uint8_t* src;       // next source row of the CTA footprint (16-B aligned down)
   const float4* wr;         // its weight record
   int64_t pitch;
   int64_t next;             // next item to open
   int rows, nbytes;         // rows left in the current item, bytes copied per row
 };
-static_assert(sizeof(TeamProd) <= 3 * sizeof(int4), "TeamProd");
+static_assert(sizeof(TeamProd) <= 48, "TeamProd");
 
-// Slice geometry of an item: output columns [j0, j0+jn), footprint pixels [pa, pa+np) with pa a multiple of 4.
 struct TItem {
   int j;                    // position in the variant list
   int k;                    // clip index
   int s, f;                 // slice, frame
+  int ws;                   // slice width
 };
 
-__device__ __forceinline__ TItem decode_item(const VIdx& vx, int cnt, int64_t item, const vp_clip_plan* plans, int p,
-                                             int* ws_out) {
+template <int NV, int NH>
+__device__ __forceinline__ TItem decode_item(const VIdx& vx, int cnt, int64_t item, const vp_clip_plan* plans, int p) {
   TItem t;
   t.j = vfind(vx, cnt, item);
   t.k = vx.list[t.j];
   const vp_clip_plan& pl = plans[t.k];
-  const TeamGeo g = team_geometry(pl.in_w, pl.out_w, p);
+  t.ws = team_geometry(pl.in_w, pl.out_w, p, NV, NH).ws;
   const int64_t local = item - vx.off[t.j];
   t.s = (int)(local / pl.n_frames);            // slice-major: consecutive items share the slice's H weights
   t.f = (int)(local - (int64_t)t.s * pl.n_frames);
-  *ws_out = g.ws;
   return t;
 }
 
+// Slice span: output columns [j0, j0+jn), footprint pixels [pa, pa+np) with pa a multiple of 4.
 __device__ __forceinline__ void slice_span(const vp_clip_plan& pl, int ws, int s, int& j0, int& jn, int& pa, int& np) {
   j0 = s * ws;
   jn = min(ws, pl.out_w - j0);
@@ -95,12 +104,9 @@ __device__ __forceinline__ void slice_span(const vp_clip_plan& pl, int ws, int s
 
 __device__ __forceinline__ float2& h2(float4& v, int h) { return reinterpret_cast<float2*>(&v)[h]; }
 
-// Retired-row swizzle (pixel-major float4 at vpos(x)): inside each 32-pixel block, sub-pixel-major (pixel 4a+k at
+// Retired-row swizzle (pixel-major float4 at tpos(x)): inside each 32-pixel block, sub-pixel-major (pixel 4a+k at
 // 8k+a) -- the V lanes' stores (pixels 4L+k) hit 8 distinct 16-B granules per quarter-warp.
-__device__ __forceinline__ int tpos(int x) {
-  x &= kTPx - 1;
-  return (x & ~31) | ((x & 3) << 3) | ((x & 31) >> 2);
-}
+__device__ __forceinline__ int tpos(int x) { return (x & ~31) | ((x & 3) << 3) | ((x & 31) >> 2); }
 
 // bytes -> floats: I2F.U8 (XU pipe) or PRMT into 2^23 + b then FADD2 -2^23 (ALU + FMA pipes); both exact.
 __device__ __forceinline__ void cvt_i2f(uint32_t w, float2& lo, float2& hi) {
@@ -113,6 +119,24 @@ __device__ __forceinline__ void cvt_magic(uint32_t w, float2& lo, float2& hi) {
                               __uint_as_float(__byte_perm(w, 0x4B000000u, 0x7541u))), mm);
   hi = __fadd2_rn(make_float2(__uint_as_float(__byte_perm(w, 0x4B000000u, 0x7542u)),
                               __uint_as_float(__byte_perm(w, 0x4B000000u, 0x7543u))), mm);
+}
+
+// A lane's 12 staged bytes (R0 G0 B0 R1 | G1 B1 R2 G2 | B2 R3 G3 B3 in words n0, n1, n2) as the six FFMA2 operand
+// pairs of the ring, ordered so that the accumulator quads are (R0 G0 B0 R3), (R1 G1 B1 G3), (R2 G2 B2 B3): pixels
+// 0..2 retire as whole quads (their .w is pixel 3's channel, ignored by the horizontal pass) and pixel 3 is the .w
+// column.  8 bytes convert on the XU pipe (I2F.U8 with a byte select), 4 on ALU + FMA (PRMT + FADD2).
+__device__ __forceinline__ float byte_i2f(uint32_t w, int k) { return (float)((w >> (8 * k)) & 0xffu); }
+__device__ __forceinline__ float byte_magic(uint32_t w, int k) {      // 2^23 + b (exact)
+  return __uint_as_float(__byte_perm(w, 0x4B000000u, 0x7540u + (unsigned)k));
+}
+__device__ __forceinline__ void cvt_ring(uint32_t n0, uint32_t n1, uint32_t n2, float2 (&f)[6]) {
+  const float2 mm = make_float2(-8388608.f, -8388608.f);
+  f[0] = make_float2(byte_i2f(n0, 0), byte_i2f(n0, 1));                                   // R0 G0
+  f[1] = __fadd2_rn(make_float2(byte_magic(n0, 2), byte_magic(n2, 1)), mm);               // B0 R3
+  f[2] = make_float2(byte_i2f(n0, 3), byte_i2f(n1, 0));                                   // R1 G1
+  f[3] = __fadd2_rn(make_float2(byte_magic(n1, 1), byte_magic(n2, 2)), mm);               // B1 G3
+  f[4] = make_float2(byte_i2f(n1, 2), byte_i2f(n1, 3));                                   // R2 G2
+  f[5] = make_float2(byte_i2f(n2, 0), byte_i2f(n2, 3));                                   // B2 B3
 }
 
 // One source row into the ring: output rows i..i+3 (i in slot U) get weights w.x..w.w.
@@ -165,21 +189,26 @@ __device__ __forceinline__ void store_pair(const FKParams& kp, char* q, float2 a
   }
 }
 
-#ifndef VP_TEAM_MINB
-#define VP_TEAM_MINB 3      // CTAs per SM the register budget is sized for (3: 168 registers, no spills)
-#endif
-template <int kUL, bool kF32, int P, int M, int TP>
-__global__ void __launch_bounds__(kTT, VP_TEAM_MINB)
-resize_team_kernel(FKParams kp, const vp_clip_plan* __restrict__ plans, const VIdx vx, const int* __restrict__ tab_alias,
-                   const int* __restrict__ tab_flag, const float4* __restrict__ vtab, const int* __restrict__ y1tab, const uint8_t* __restrict__ frames,
-                   const int64_t* __restrict__ clip_off, const int64_t* __restrict__ pitch_arr, void* pv_img,
-                   int64_t img_cap, void* pv_vid, int64_t vid_cap, int32_t* __restrict__ clip_status) {
-  __shared__ __align__(128) TeamSmem sm;
+template <int NV, int NH, int PPL, int kUL, bool kF32, int P, int M, int TP, int MINB>
+__global__ void __launch_bounds__((NV + NH) * 32, MINB)
+resize_split_kernel(FKParams kp, const vp_clip_plan* __restrict__ plans, const VIdx vx, const int* __restrict__ tab_alias,
+                    const int* __restrict__ tab_flag, const float4* __restrict__ vtab, const int* __restrict__ y1tab,
+                    const uint8_t* __restrict__ frames, const int64_t* __restrict__ clip_off,
+                    const int64_t* __restrict__ pitch_arr, void* pv_img, int64_t img_cap, void* pv_vid, int64_t vid_cap,
+                    int32_t* __restrict__ clip_status) {
+  using Cfg = SplitCfg<NV, NH>;
+  constexpr int kPx = Cfg::kPx;
+  constexpr int kRowB = Cfg::kRowB;
+  // preset geometry (p % 4 == 0 and p*m % 4 == 0): every out_h is a multiple of 4, so with 4 retire slots the slot of
+  // output row i is i % 4 = the static unroll index U
+  constexpr bool kStatic = P > 0 && (P % 4) == 0 && ((P * M) % 4) == 0 && kNR == 4;
+  extern __shared__ __align__(128) unsigned char smem[];
   const int tid = threadIdx.x;
   const int warp = __shfl_sync(0xffffffffu, tid >> 5, 0);
   int lane;
   asm volatile("mov.u32 %0, %%laneid;" : "=r"(lane));
   const bool l0 = lane == 0;
+  const int p = P > 0 ? P : kp.p, m = P > 0 ? M : kp.m, tp = P > 0 ? TP : kp.tp;
 
   const int cnt = (int)vx.meta[0];
   const int64_t total = vx.meta[1];
@@ -187,39 +216,29 @@ resize_team_kernel(FKParams kp, const vp_clip_plan* __restrict__ plans, const VI
   const int64_t my_b = total * (blockIdx.x + 1) / gridDim.x;
   if (my_a >= my_b) return;
 
-  if (tid == 0) {
-    for (int w = 0; w < kTW; ++w)
-      for (int g = 0; g < kTNGrp; ++g) mbar_init(&sm.full[w][g], 1);
-    asm volatile("fence.mbarrier_init.release.cluster;" ::: "memory");
-  }
-  for (int i = tid; i < 2 * kTPx; i += kTT) (&sm.buf[0][0])[i] = make_float4(0.f, 0.f, 0.f, 0.f);
-  __syncthreads();
+  uint8_t* stage = smem + Cfg::OFF_STG;
+  float4* wrec = reinterpret_cast<float4*>(smem + Cfg::OFF_WREC);
+  uint64_t* sfull = reinterpret_cast<uint64_t*>(smem + Cfg::OFF_SBAR);      // staging group landed (TMA tx)
+  uint64_t* rfull = reinterpret_cast<uint64_t*>(smem + Cfg::OFF_RBAR);      // V -> H: retire slot filled
+  uint64_t* rempty = rfull + kNR;                                           // H -> V: retire slot released
+  int* gcnt = reinterpret_cast<int*>(smem + Cfg::OFF_CNT);                  // V warps done with a staging group
+  TeamProd* ps = reinterpret_cast<TeamProd*>(smem + Cfg::OFF_PROD);
+  float4* buf0 = reinterpret_cast<float4*>(smem + Cfg::OFF_BUF);
+  const uint32_t buf_s = smem_u32(buf0);
+  constexpr uint32_t kSlotB = (uint32_t)kPx * 16;     // bytes per retire slot
 
-  // ------------------------------------------------------------------ producer (this warp's part)
-  uint8_t* stage = &sm.stage[warp][0][0];
-  float4* wrec = &sm.wrec[warp][0];
-  uint64_t* full = &sm.full[warp][0];
-  TeamProd* ps = reinterpret_cast<TeamProd*>(&sm.prod[warp][0]);
-  if (l0) {
-    TeamProd z;
-    z.src = nullptr; z.wr = nullptr; z.pitch = 0; z.next = my_a; z.rows = 0; z.nbytes = 0;
-    *ps = z;
-  }
-  __syncwarp();
-  auto open_item = [&](TeamProd& st) {          // warp-uniform
-    int ws;
-    const TItem t = decode_item(vx, cnt, st.next, plans, P > 0 ? P : kp.p, &ws);
+  // ---- staging producer: refill group g with the next kTGrp source rows of the CTA's item sequence (warp-uniform
+  //      caller; the copies and barrier operations are predicated to lane 0) ----
+  auto open_item = [&](TeamProd& st) {
+    const TItem t = decode_item<NV, NH * PPL>(vx, cnt, st.next, plans, p);
     const vp_clip_plan& pl = plans[t.k];
     int j0, jn, pa, np;
-    slice_span(pl, ws, t.s, j0, jn, pa, np);
-    const int px0 = pa + warp * 128;
-    const int pxn = min(128, np - warp * 128);
-    const int b0 = 3 * px0;
-    const int o = b0 & 15;
-    st.nbytes = pxn > 0 ? ((o + 3 * pxn + 15) & ~15) : 0;
+    slice_span(pl, t.ws, t.s, j0, jn, pa, np);
+    const int b0 = 3 * pa, o = b0 & 15;
+    st.nbytes = (o + 3 * np + 15) & ~15;
     st.pitch = pitch_arr[t.k];
     st.src = frames + clip_off[t.k] + (int64_t)t.f * pl.in_h * st.pitch + (b0 - o);
-    st.wr = vtab + (int64_t)tab_alias[t.j] * kTabInH;
+    st.wr = vtab + (int64_t)tab_alias[t.k] * kTabInH;
     st.rows = pl.in_h;
     ++st.next;
   };
@@ -227,12 +246,12 @@ resize_team_kernel(FKParams kp, const vp_clip_plan* __restrict__ plans, const VI
     asm volatile("mov.b32 %0, %0;" : "+r"(g));   // opaque copy (nvcc 12.9 mbarrier-address CSE workaround)
     TeamProd st = *ps;
     if (st.rows >= kTGrp) {
-      mbar_expect_tx_if(&full[g], (uint32_t)(kTGrp * st.nbytes + kTGrp * 16), l0);
+      mbar_expect_tx_if(&sfull[g], (uint32_t)(kTGrp * st.nbytes + kTGrp * 16), l0);
 #pragma unroll
       for (int q = 0; q < kTGrp; ++q)
-        tma_bulk_g2s_if(stage + (size_t)(g * kTGrp + q) * kTRowB, st.src + (int64_t)q * st.pitch, (uint32_t)st.nbytes,
-                        &full[g], l0 && st.nbytes > 0);
-      tma_bulk_g2s_if(wrec + g * kTGrp, st.wr, kTGrp * 16, &full[g], l0);
+        tma_bulk_g2s_if(stage + (size_t)(g * kTGrp + q) * kRowB, st.src + (int64_t)q * st.pitch, (uint32_t)st.nbytes,
+                        &sfull[g], l0);
+      tma_bulk_g2s_if(wrec + g * kTGrp, st.wr, kTGrp * 16, &sfull[g], l0);
       st.src += (int64_t)kTGrp * st.pitch;
       st.wr += kTGrp;
       st.rows -= kTGrp;
@@ -241,189 +260,230 @@ resize_team_kernel(FKParams kp, const vp_clip_plan* __restrict__ plans, const VI
       for (int q = 0; q < kTGrp; ++q) {
         if (st.rows == 0 && st.next < my_b) open_item(st);
         if (st.rows > 0) {
-          mbar_expect_tx_if(&full[g], (uint32_t)(st.nbytes + 16), l0);
-          tma_bulk_g2s_if(stage + (size_t)(g * kTGrp + q) * kTRowB, st.src, (uint32_t)st.nbytes, &full[g],
-                          l0 && st.nbytes > 0);
-          tma_bulk_g2s_if(wrec + g * kTGrp + q, st.wr, 16, &full[g], l0);
+          mbar_expect_tx_if(&sfull[g], (uint32_t)(st.nbytes + 16), l0);
+          tma_bulk_g2s_if(stage + (size_t)(g * kTGrp + q) * kRowB, st.src, (uint32_t)st.nbytes, &sfull[g], l0);
+          tma_bulk_g2s_if(wrec + g * kTGrp + q, st.wr, 16, &sfull[g], l0);
           st.src += st.pitch;
           st.wr += 1;
           --st.rows;
         }
       }
     }
-    mbar_arrive_if(&full[g], l0);
+    mbar_arrive_if(&sfull[g], l0);
     __syncwarp();
     if (l0) *ps = st;
     __syncwarp();
   };
-  for (uint32_t g = 0; g < kTNGrp; ++g) issue_group(g);
 
-  // ------------------------------------------------------------------ consumer
-  // model geometry: compile-time for the preset instantiations (P > 0), runtime otherwise
-  const int p = P > 0 ? P : kp.p, m = P > 0 ? M : kp.m, tp = P > 0 ? TP : kp.tp;
+  if (tid == 0) {
+    for (int i = 0; i < kTNGrp; ++i) { mbar_init(&sfull[i], 1); gcnt[i] = 0; }
+    for (int i = 0; i < kNR; ++i) {
+      mbar_init(&rfull[i], NV);
+      mbar_init(&rempty[i], NH);
+    }
+    asm volatile("fence.mbarrier_init.release.cluster;" ::: "memory");
+    TeamProd z;
+    z.src = nullptr; z.wr = nullptr; z.pitch = 0; z.next = my_a; z.rows = 0; z.nbytes = 0;
+    *ps = z;
+  }
+  for (int i = tid; i < kNR * kPx; i += Cfg::kThreads) buf0[i] = make_float4(0.f, 0.f, 0.f, 0.f);
+  __syncthreads();
+  if (warp == 0)
+    for (uint32_t g = 0; g < kTNGrp; ++g) issue_group(g);   // prefill
+
+  if (warp < NV) {
+    // ================================================================= V warps
+    const uint32_t stage_s = smem_u32(stage), wrec_s = smem_u32(wrec);
+    // retire address of this lane's 4 pixels (pixel 128*warp + 4*lane + k at +128k) in retire slot 0
+    const uint32_t vsa = buf_s + (uint32_t)tpos(warp * 128 + lane * 4) * 16u;
+    uint32_t rc = 0;                              // staged rows consumed: slot rc % kTDepth
+    uint32_t rr = 0;                              // output rows retired (all items)
+    for (int64_t item = my_a; item < my_b; ++item) {
+      const TItem t = decode_item<NV, NH * PPL>(vx, cnt, item, plans, p);
+      const vp_clip_plan& pl = plans[t.k];
+      const int in_h = pl.in_h, out_h = pl.out_h;
+      const int pa = window_of(pl.in_w, pl.out_w, t.s * t.ws).x0 & ~3;
+      const int* y1 = y1tab + (int64_t)tab_alias[t.k] * kTabOutH;
+      // byte offset of this lane's 12 bytes inside a staged row (the footprint starts at (3*pa) & 15)
+      const uint32_t lofs = (uint32_t)(((3 * pa) & 15) + 384 * warp + 12 * lane);
+      float4 acc[4][3];
+#pragma unroll
+      for (int r = 0; r < 4; ++r)
+#pragma unroll
+        for (int q = 0; q < 3; ++q) acc[r][q] = make_float4(0.f, 0.f, 0.f, 0.f);
+      int y = 0;
+      // after the last row of group g: the last V warp to finish it refills it
+      auto group_done = [&](uint32_t g) {
+        __syncwarp();
+        int old = 0;
+        if (l0) {
+          __threadfence_block();
+          old = atomicAdd(&gcnt[g], 1);
+          if (old == NV - 1) gcnt[g] = 0;
+        }
+        if (__shfl_sync(0xffffffffu, old, 0) == NV - 1) issue_group(g);
+      };
+#define VP_V_BODY(U)                                                                                         \
+      {                                                                                                       \
+        if ((rc & (kTGrp - 1)) == 0) mbar_wait_uni(&sfull[(rc / kTGrp) % kTNGrp], (rc / kTDepth) & 1);        \
+        const uint32_t slot = rc % kTDepth;                                                                   \
+        const uint32_t sa = stage_s + slot * kRowB + lofs;                                                    \
+        const uint32_t n0 = lds_u32(sa), n1 = lds_u32(sa + 4), n2 = lds_u32(sa + 8);                          \
+        const float4 wv = lds_f4(wrec_s + slot * 16);                                                         \
+        float2 fv[6];                                                                                         \
+        cvt_ring(n0, n1, n2, fv);                                                                             \
+        ++rc;                                                                                                 \
+        if ((slot & (kTGrp - 1)) == kTGrp - 1) group_done(slot / kTGrp);                                      \
+        ring4<U>(acc, wv, fv);                                                                                \
+      }
+#define VP_V_RETIRE(U)                                                                                       \
+      {                                                                                                       \
+        const uint32_t rs = kStatic ? (uint32_t)U : rr % kNR;                                                 \
+        mbar_wait_uni<VP_TEAM_HINT>(&rempty[rs], ((rr / kNR) & 1) ^ 1);                                       \
+        const uint32_t ra = vsa + rs * kSlotB;                                                                \
+        const float4* a = acc[U];                     /* pixels 0..2 are quads .xyz; pixel 3 is the .w column */ \
+        sts_f4(ra, a[0]);                                                                                     \
+        sts_f4(ra + 128, a[1]);                                                                               \
+        sts_f4(ra + 256, a[2]);                                                                               \
+        sts_f4(ra + 384, make_float4(a[0].w, a[1].w, a[2].w, 0.f));                                           \
+        _Pragma("unroll") for (int q = 0; q < 3; ++q) acc[U][q] = make_float4(0.f, 0.f, 0.f, 0.f);            \
+        __syncwarp();                                                                                         \
+        mbar_arrive_if(&rfull[rs], l0);                                                                       \
+        ++rr;                                                                                                 \
+      }
+      int4 ye_next = __ldg(reinterpret_cast<const int4*>(y1));
+      for (int ib = 0; ib < out_h; ib += 4) {
+        const int4 ye = ye_next;                  // window ends of rows ib..ib+3, prefetched one group ahead
+        if (ib + 4 < out_h) ye_next = __ldg(reinterpret_cast<const int4*>(y1 + ib + 4));
+#define VP_V_ROW(U, YE)                                                                                      \
+        if (kStatic || ib + U < out_h) {                                                                      \
+          const int yend = YE;                                                                                \
+          for (; y < yend; ++y) VP_V_BODY(U)                                                                  \
+          VP_V_RETIRE(U)                                                                                      \
+        }
+        VP_V_ROW(0, ye.x)
+        VP_V_ROW(1, ye.y)
+        VP_V_ROW(2, ye.z)
+        VP_V_ROW(3, ye.w)
+#undef VP_V_ROW
+      }
+      // source rows below the last window (zero weights): keep the staging ring in step
+      for (; y < in_h; ++y) {
+        if ((rc & (kTGrp - 1)) == 0) mbar_wait_uni(&sfull[(rc / kTGrp) % kTNGrp], (rc / kTDepth) & 1);
+        const uint32_t slot = rc % kTDepth;
+        ++rc;
+        if ((slot & (kTGrp - 1)) == kTGrp - 1) group_done(slot / kTGrp);
+      }
+#undef VP_V_BODY
+#undef VP_V_RETIRE
+    }
+    return;
+  }
+
+  // =================================================================== H warps
+  const int hw = warp - NV;
   const int B = m * p, D = 3 * tp * p * p;
   const int cstride = tp * p * p;                 // elements between channel blocks of a patch row (O8)
   constexpr int kEsz = kF32 ? 4 : 2;
-  uint32_t rc = 0;                                // staged rows consumed: slot rc % kTDepth
   int cur_j = -1, cur_s = -1;
-  // per-slice H state (registers): pair weights and swizzled tap shared addresses
-  float2 wp[kUL];
-  uint32_t toff[kUL];                             // shared addresses of the taps in retire buffer 0
-  int colpart = 0;
-  bool hact = false;
-  const uint32_t buf_s = smem_u32(&sm.buf[0][0]);
-  // V retire address of this lane's 4 pixels (pixel 128*warp + 4*lane + k at +128k)
-  const uint32_t vsa = buf_s + (uint32_t)tpos(warp * 128 + lane * 4) * 16u;
-  const uint32_t stage_s = smem_u32(stage), wrec_s = smem_u32(wrec);
-
+  float2 wp[PPL][kUL];                            // pair weights per union tap
+  uint32_t toff[PPL][kUL];                        // shared addresses of the taps in retire slot 0
+  int colpart[PPL];
+  bool hact[PPL];
+  uint32_t rr = 0;
   for (int64_t item = my_a; item < my_b; ++item) {
-    int ws;
-    const TItem t = decode_item(vx, cnt, item, plans, p, &ws);
+    const TItem t = decode_item<NV, NH * PPL>(vx, cnt, item, plans, p);
     const vp_clip_plan& pl = plans[t.k];
-    const int in_h = pl.in_h, out_h = pl.out_h;
-    int j0, jn, pa, np;
-    slice_span(pl, ws, t.s, j0, jn, pa, np);
-    const int ta = tab_alias[t.j];
-    const int* y1 = y1tab + (int64_t)ta * kTabOutH;
-    if (tid == 0 && tab_flag[ta] != 0 && clip_status != nullptr) clip_status[t.k] = VP_EUNSUPPORTED;
+    const int out_h = pl.out_h;
+    if (hw == 0 && l0 && tab_flag[tab_alias[t.k]] != 0 && clip_status != nullptr) clip_status[t.k] = VP_EUNSUPPORTED;
     if (t.j != cur_j || t.s != cur_s) {
-      // ---- K2 for this slice: union window of my column pair, f64 Keys / f64 sums -> fp32 ----
+      // ---- K2 for this slice: union window of each of my column pairs, f64 Keys / f64 sums -> fp32 ----
       cur_j = t.j;
       cur_s = t.s;
-      const int q = warp * 32 + lane;
-      hact = 2 * q < jn;
-      const int ja = j0 + 2 * min(q, max(jn / 2 - 1, 0));
-      const Win w0 = window_of(pl.in_w, pl.out_w, ja);
-      const Win w1 = window_of(pl.in_w, pl.out_w, ja + 1);
-      double s0 = 0.0, s1 = 0.0;
-      for (int x = w0.x0; x < w0.x1; ++x) s0 += keys_d(((double)x - w0.c + 0.5) * w0.inv);
-      for (int x = w1.x0; x < w1.x1; ++x) s1 += keys_d(((double)x - w1.c + 0.5) * w1.inv);
-      const double r0 = s0 != 0.0 ? s0 : 1.0, r1 = s1 != 0.0 ? s1 : 1.0;
-      const int xu = min(w0.x0, w1.x0);
-      if (hact && max(w0.x1, w1.x1) - xu > kUL && clip_status != nullptr) clip_status[t.k] = VP_EUNSUPPORTED;
+      int j0, jn, pa, np;
+      slice_span(pl, t.ws, t.s, j0, jn, pa, np);
 #pragma unroll
-      for (int u = 0; u < kUL; ++u) {
-        const int x = xu + u;
-        const float wa = (x >= w0.x0 && x < w0.x1) ? (float)(keys_d(((double)x - w0.c + 0.5) * w0.inv) / r0) : 0.f;
-        const float wb = (x >= w1.x0 && x < w1.x1) ? (float)(keys_d(((double)x - w1.c + 0.5) * w1.inv) / r1) : 0.f;
-        wp[u] = make_float2(wa, wb);
-        toff[u] = buf_s + (uint32_t)tpos(x - pa) * 16u;
+      for (int pp = 0; pp < PPL; ++pp) {
+        const int q = pp * NH * 32 + hw * 32 + lane;
+        hact[pp] = 2 * q < jn;
+        const int ja = j0 + 2 * min(q, max(jn / 2 - 1, 0));
+        const Win w0 = window_of(pl.in_w, pl.out_w, ja);
+        const Win w1 = window_of(pl.in_w, pl.out_w, ja + 1);
+        double s0 = 0.0, s1 = 0.0;
+        for (int x = w0.x0; x < w0.x1; ++x) s0 += keys_d(((double)x - w0.c + 0.5) * w0.inv);
+        for (int x = w1.x0; x < w1.x1; ++x) s1 += keys_d(((double)x - w1.c + 0.5) * w1.inv);
+        const double r0 = s0 != 0.0 ? s0 : 1.0, r1 = s1 != 0.0 ? s1 : 1.0;
+        const int xu = min(w0.x0, w1.x0);
+        if (hact[pp] && max(w0.x1, w1.x1) - xu > kUL && clip_status != nullptr) clip_status[t.k] = VP_EUNSUPPORTED;
+#pragma unroll
+        for (int u = 0; u < kUL; ++u) {
+          const int x = xu + u;
+          const float wa = (x >= w0.x0 && x < w0.x1) ? (float)(keys_d(((double)x - w0.c + 0.5) * w0.inv) / r0) : 0.f;
+          const float wb = (x >= w1.x0 && x < w1.x1) ? (float)(keys_d(((double)x - w1.c + 0.5) * w1.inv) / r1) : 0.f;
+          wp[pp][u] = make_float2(wa, wb);
+          toff[pp][u] = buf_s + (uint32_t)tpos(min(x - pa, kPx - 1)) * 16u;   // slack taps (weight 0) stay in the row
+        }
+        const int jl0 = ja % B, wbk = ja / B, mw = jl0 / p, px = jl0 - mw * p;
+        colpart[pp] = (wbk * m * m + mw) * D + px;
       }
-      const int jl0 = ja % B, wbk = ja / B, mw = jl0 / p, px = jl0 - mw * p;
-      colpart = (wbk * m * m + mw) * D + px;
     }
     // ---- output addressing of frame f (O7, O8): element (row, q) of pixel_values at row*D + q ----
     void* pv = pl.is_image ? pv_img : pv_vid;
     const int64_t cap = pl.is_image ? img_cap : vid_cap;
     const bool writable = pv != nullptr && pl.patch_offset + (int64_t)pl.grid_t * pl.grid_h * pl.grid_w <= cap;
-    const bool hst = writable && hact;
     const int f = t.f;
     const int last_slot = (f == pl.n_frames - 1) ? pl.grid_t * tp - 1 : f;     // frame n-1 fills the pad slots
     const int nslots = last_slot - f + 1;
     const int g0 = f / tp, ti0 = f - g0 * tp;
     const int64_t group_stride = (int64_t)(pl.grid_h / m) * (pl.grid_w / m) * m * m * D;
     const int hb_stride = (pl.grid_w / m) * m * m * D;        // one merge-row band of one temporal group
-    // this lane's first element of frame f's slot: row offsets are added per output row
-    char* const lbase = reinterpret_cast<char*>(pv) +
-        (pl.patch_offset * (int64_t)D + (int64_t)g0 * group_stride + (int64_t)ti0 * p * p + colpart) * kEsz;
-
-    float4 acc[4][3];
+    char* const fbase = reinterpret_cast<char*>(pv) +
+        (pl.patch_offset * (int64_t)D + (int64_t)g0 * group_stride + (int64_t)ti0 * p * p) * kEsz;
+    bool hst[PPL];
 #pragma unroll
-    for (int r = 0; r < 4; ++r)
+    for (int pp = 0; pp < PPL; ++pp) hst[pp] = writable && hact[pp];
+    auto hrow = [&](uint32_t so, int ro) {          // H of one retired row in slot offset so, output row offset ro
 #pragma unroll
-      for (int q = 0; q < 3; ++q) acc[r][q] = make_float4(0.f, 0.f, 0.f, 0.f);
-    // byte offset of this lane's 12 bytes inside a staged row (the part starts at (3*pa) & 15)
-    const uint32_t lofs = (uint32_t)(((3 * pa) & 15) + 12 * lane);
-
-    int y = 0;
-    // one source row into the ring (output row ib+U being completed sits in slot U)
-    // staged row rc: bytes n0..n2 and weight record wv (after its group's TMA landed)
-    uint32_t n0, n1, n2;
-    float4 wv;
-    auto load_row = [&]() {
-      if ((rc & (kTGrp - 1)) == 0) mbar_wait(&full[(rc / kTGrp) % kTNGrp], (rc / kTDepth) & 1);
-      const uint32_t slot = rc % kTDepth;
-      const uint32_t sa = stage_s + slot * kTRowB + lofs;
-      n0 = lds_u32(sa); n1 = lds_u32(sa + 4); n2 = lds_u32(sa + 8);
-      wv = lds_f4(wrec_s + slot * 16);
+      for (int pp = 0; pp < PPL; ++pp) {
+        if (hst[pp]) {
+          float2 ar = make_float2(0.f, 0.f), ag = ar, ab = ar;
+#pragma unroll
+          for (int u = 0; u < kUL; ++u) {
+            const float4 v = lds_f4(toff[pp][u] + so);
+            ar = __ffma2_rn(make_float2(v.x, v.x), wp[pp][u], ar);
+            ag = __ffma2_rn(make_float2(v.y, v.y), wp[pp][u], ag);
+            ab = __ffma2_rn(make_float2(v.z, v.z), wp[pp][u], ab);
+          }
+          store_pair<kF32>(kp, fbase + (int64_t)(ro + colpart[pp]) * kEsz, ar, ag, ab, cstride, nslots, ti0, tp, p,
+                           group_stride);
+        }
+      }
     };
-    if (VP_TEAM_PF) load_row();
-#define VP_TEAM_BODY(U)                                                                                      \
-    {                                                                                                         \
-      if (!VP_TEAM_PF) load_row();                                                                            \
-      const uint32_t slot = rc % kTDepth;                                                                     \
-      float2 fv[6];                                                                                           \
-      cvt_i2f(n0, fv[0], fv[1]);                                                                              \
-      cvt_i2f(n1, fv[2], fv[3]);                                                                              \
-      cvt_magic(n2, fv[4], fv[5]);                                                                            \
-      const float4 wc = wv;                                                                                   \
-      ++rc;                                                                                                   \
-      if ((slot & (kTGrp - 1)) == kTGrp - 1) {                                                                \
-        __syncwarp();                                                                                         \
-        issue_group(slot / kTGrp);                                                                            \
-      }                                                                                                       \
-      if (VP_TEAM_PF) load_row();                                                                             \
-      ring4<U>(acc, wc, fv);                                                                                  \
-    }
-
-    // retire output row i = ib + U from slot U into buffer U & 1, barrier, H of row i.  Row offset of output
-    // row i (O8): (i / (m p)) * hb_stride + ((i / p) % m) * m * D + (i % p) * p; for the preset (p % 4 == 0) the
-    // 4 rows of a group share i / p, so row ib+U is the group's offset + U*p (an immediate).
-#define VP_TEAM_RETIRE(U)                                                                                    \
-    {                                                                                                         \
-      const uint32_t ra = vsa + (U & 1) * kTPx * 16;                                                          \
-      const float4* a = acc[U];                                                                               \
-      sts_f4(ra, a[0]);                                                                                       \
-      sts_f4(ra + 128, make_float4(a[0].w, a[1].x, a[1].y, 0.f));                                             \
-      sts_f4(ra + 256, make_float4(a[1].z, a[1].w, a[2].x, a[2].y));                                          \
-      sts_f4(ra + 384, make_float4(a[2].y, a[2].z, a[2].w, 0.f));                                             \
-      _Pragma("unroll") for (int q = 0; q < 3; ++q) acc[U][q] = make_float4(0.f, 0.f, 0.f, 0.f);              \
-      __syncthreads();                                                                                        \
-      if (hst) {                                                                                              \
-        float2 ar = make_float2(0.f, 0.f), ag = ar, ab = ar;                                                  \
-        _Pragma("unroll") for (int u = 0; u < kUL; ++u) {                                                     \
-          const float4 v = lds_f4(toff[u] + (U & 1) * kTPx * 16);                                             \
-          ar = __ffma2_rn(make_float2(v.x, v.x), wp[u], ar);                                                  \
-          ag = __ffma2_rn(make_float2(v.y, v.y), wp[u], ag);                                                  \
-          ab = __ffma2_rn(make_float2(v.z, v.z), wp[u], ab);                                                  \
-        }                                                                                                     \
-        const int i = ib + U;                                                                                 \
-        const int ro = (P > 0 && (P & 3) == 0) ? ro_grp + U * p                                               \
-                                               : (i / B) * hb_stride + ((i / p) % m) * m * D + (i % p) * p;  \
-        store_pair<kF32>(kp, lbase + (int64_t)ro * kEsz, ar, ag, ab, cstride, nslots, ti0, tp, p, group_stride);\
-      }                                                                                                       \
-    }
-
-    int4 ye_next = __ldg(reinterpret_cast<const int4*>(y1));
-    for (int ib = 0; ib < out_h; ib += 4) {
-      const int4 ye = ye_next;                    // window ends of rows ib..ib+3, prefetched one group ahead
-      if (ib + 4 < out_h) ye_next = __ldg(reinterpret_cast<const int4*>(y1 + ib + 4));
-      const int ro_grp = (ib / B) * hb_stride + ((ib / p) % m) * m * D + (ib % p) * p;
-#define VP_TEAM_ROW(U, YE)                                                                                   \
-      if (ib + U < out_h) {                                                                                   \
-        const int yend = YE;                                                                                  \
-        for (; y < yend; ++y) VP_TEAM_BODY(U)                                                                 \
-        VP_TEAM_RETIRE(U)                                                                                     \
+    if (kStatic) {
+      for (int ib = 0; ib < out_h; ib += 4) {
+        // row offset of output row i (O8): (i / (m p)) * hb_stride + ((i / p) % m) * m * D + (i % p) * p; the 4 rows
+        // of a group share i / p
+        const int ro_grp = (ib / B) * hb_stride + ((ib / p) % m) * m * D + (ib % p) * p;
+        const uint32_t par = (rr / kNR) & 1;
+#pragma unroll
+        for (int U = 0; U < 4; ++U) {
+          mbar_wait_uni<VP_TEAM_HINT>(&rfull[U], par);
+          hrow((uint32_t)U * kSlotB, ro_grp + U * p);
+          __syncwarp();
+          mbar_arrive_if(&rempty[U], l0);
+        }
+        rr += 4;
       }
-      VP_TEAM_ROW(0, ye.x)
-      VP_TEAM_ROW(1, ye.y)
-      VP_TEAM_ROW(2, ye.z)
-      VP_TEAM_ROW(3, ye.w)
-#undef VP_TEAM_ROW
-    }
-    // source rows below the last window (zero weights): keep the staging ring in step
-    for (; y < in_h; ++y) {
-      if (!VP_TEAM_PF && (rc & (kTGrp - 1)) == 0) mbar_wait(&full[(rc / kTGrp) % kTNGrp], (rc / kTDepth) & 1);
-      const uint32_t slot = rc % kTDepth;
-      ++rc;
-      if ((slot & (kTGrp - 1)) == kTGrp - 1) {
+    } else {
+      for (int i = 0; i < out_h; ++i) {
+        const uint32_t rs = rr % kNR;
+        mbar_wait_uni<VP_TEAM_HINT>(&rfull[rs], (rr / kNR) & 1);
+        hrow(rs * kSlotB, (i / B) * hb_stride + ((i / p) % m) * m * D + (i % p) * p);
         __syncwarp();
-        issue_group(slot / kTGrp);
+        mbar_arrive_if(&rempty[rs], l0);
+        ++rr;
       }
-      if (VP_TEAM_PF && (rc & (kTGrp - 1)) == 0) mbar_wait(&full[(rc / kTGrp) % kTNGrp], (rc / kTDepth) & 1);
     }
-#undef VP_TEAM_BODY
-#undef VP_TEAM_RETIRE
   }
 }
 
@@ -438,12 +498,18 @@ __device__ __forceinline__ double win_sum(const Win& w) {
   return s;
 }
 
+__device__ __forceinline__ bool teamish(const vp_clip_plan& pl, int64_t coff, int64_t pitch) {
+  return pl.status == VP_OK && pl.tile_count > 0 && (pl.kernel_variant == KV_TEAM || pl.kernel_variant == KV_WIDE) &&
+         ((coff | pitch) & 15) == 0;
+}
+
 __global__ void __launch_bounds__(128)
-team_vtab_kernel(const vp_clip_plan* __restrict__ plans, const VIdx vx, const int* __restrict__ alias,
-                 float4* __restrict__ vtab, int* __restrict__ y1tab, int* __restrict__ tflag) {
-  const int j = blockIdx.y;
-  if (j >= (int)vx.meta[0] || alias[j] != j) return;
-  const vp_clip_plan& pl = plans[vx.list[j]];
+team_vtab_kernel(const vp_clip_plan* __restrict__ plans, const int64_t* __restrict__ coff,
+                 const int64_t* __restrict__ pitch, const int* __restrict__ alias, float4* __restrict__ vtab,
+                 int* __restrict__ y1tab, int* __restrict__ tflag) {
+  const int j = blockIdx.y;                       // clip index (tables are indexed by the run's first clip)
+  const vp_clip_plan& pl = plans[j];
+  if (!teamish(pl, coff[j], pitch[j]) || alias[j] != j) return;
   const int in_h = pl.in_h, out_h = pl.out_h;
   const int r = blockIdx.x * blockDim.x + threadIdx.x;
   if (r < ((out_h + 3) & ~3)) y1tab[(int64_t)j * kTabOutH + r] = r < out_h ? window_of(in_h, out_h, r).x1 : in_h;
@@ -468,12 +534,13 @@ team_vtab_kernel(const vp_clip_plan* __restrict__ plans, const VIdx vx, const in
 }
 
 // ---------------------------------------------------------------- per-variant work index
-// One CTA: slot v in {MILD, MEDIUM, STRONG, COPY, TEAM} collects the valid, 16-B aligned clips of that variant
-// (list, batch order) and the exclusive prefix of their item counts (off); meta[v] = {count, items}.  For the
-// TEAM list, alias[j] = first position of the run of equal (in_h, out_h) that j belongs to (shared tables).
+// One CTA: slot v in {MILD, MEDIUM, STRONG, COPY, TEAM, WIDE} collects the valid, 16-B aligned clips of that
+// variant (list, batch order) and the exclusive prefix of their item counts (off); meta[v] = {count, items}.  For
+// the TEAM / WIDE clips, alias[k] = first clip of the run of consecutive such clips with equal (in_h, out_h) that k
+// belongs to: the clips of a run share one vertical table.
 constexpr int kIdxThreads = 1024;
 __device__ __forceinline__ int variant_slot(int kv) {
-  return kv == KV_COPY ? 3 : (kv == KV_TEAM ? 4 : (kv <= KV_STRONG ? kv : -1));
+  return kv == KV_COPY ? 3 : (kv == KV_TEAM ? 4 : (kv == KV_WIDE ? 5 : (kv <= KV_STRONG ? kv : -1)));
 }
 
 __global__ void __launch_bounds__(kIdxThreads)
@@ -544,21 +611,21 @@ variant_index_kernel(const vp_clip_plan* __restrict__ plans, int n, const int64_
     meta[2 * tid + 1] = c_items[tid];
   }
   __syncthreads();
-  // TEAM table aliases: inclusive max-scan of run starts over the TEAM list
-  const int nt = c_cnt[4];
-  const int* tl = list + (size_t)4 * n;
-  for (int c0 = 0; c0 < nt; c0 += kIdxThreads) {
-    const int j = c0 + tid;
+  // table aliases: inclusive max-scan of run starts over the clips
+  for (int c0 = 0; c0 < n; c0 += kIdxThreads) {
+    const int k = c0 + tid;
     int v = -1;
-    if (j < nt) {
-      tflag[j] = 0;
-      const vp_clip_plan& a = plans[tl[j]];
-      bool start = j == 0;
-      if (!start) {
-        const vp_clip_plan& b = plans[tl[j - 1]];
-        start = a.in_h != b.in_h || a.out_h != b.out_h;
+    if (k < n) {
+      tflag[k] = 0;
+      const vp_clip_plan& a = plans[k];
+      if (teamish(a, coff[k], pitch[k])) {
+        bool start = k == 0;
+        if (!start) {
+          const vp_clip_plan& b = plans[k - 1];
+          start = !teamish(b, coff[k - 1], pitch[k - 1]) || a.in_h != b.in_h || a.out_h != b.out_h;
+        }
+        v = start ? k : -1;
       }
-      v = start ? j : -1;
     }
 #pragma unroll
     for (int o = 1; o < 32; o <<= 1) v = max(v, __shfl_up_sync(0xffffffffu, v, o));
@@ -566,16 +633,24 @@ variant_index_kernel(const vp_clip_plan* __restrict__ plans, int n, const int64_
     __syncthreads();
     int pre = c_alias;
     for (int w = 0; w < warp; ++w) pre = max(pre, wmax[w]);
-    if (j < nt) alias[j] = max(pre, v);
+    if (k < n) alias[k] = max(pre, v);
     __syncthreads();
     if (tid == kIdxThreads - 1) c_alias = max(pre, v);
     __syncthreads();
   }
 }
 
-// Per-device one-time setup (thread-safe: attribute calls are idempotent, the bits only skip repeats).
+// Per-device SM-count cache (thread-safe: idempotent writes).
 constexpr int kMaxDev = 64;
 std::atomic<int> g_sms[kMaxDev];
+
+// Dynamic shared memory above 48 KB must be opted into per kernel and device; cudaFuncSetAttribute is a cheap
+// host-side call and idempotent, so it is simply made before every launch (no process state to get wrong when
+// one process drives several devices or host threads).
+template <typename K>
+void set_smem_attr(K kern, int, int bytes) {
+  cudaFuncSetAttribute(kern, cudaFuncAttributeMaxDynamicSharedMemorySize, bytes);
+}
 
 }  // namespace
 
@@ -634,20 +709,39 @@ cudaError_t launch_index(const vp_clip_plan* plans, int n, const int64_t* coff, 
   return cudaGetLastError();
 }
 
+template <int NV, int NH, int PPL, int MINB, bool kF32>
+void launch_split(const FKParams& kp, bool preset, const vp_clip_plan* plans, const VIdx& vx, const ResizeWs& w,
+                  const uint8_t* frames, const int64_t* coff, const int64_t* pitch, void* pi, int64_t icap, void* pvv,
+                  int64_t vcap, int32_t* clip_status, int dev, int num_sms, cudaStream_t s) {
+  using Cfg = SplitCfg<NV, NH>;
+  // Qwen2.5/3-VL geometry (p16 m2 tp2) with compile-time output addressing, else runtime parameters
+  auto kern = preset ? resize_split_kernel<NV, NH, PPL, kTeamUL, kF32, 16, 2, 2, MINB>
+                     : resize_split_kernel<NV, NH, PPL, kTeamUL, kF32, 0, 0, 0, MINB>;
+  set_smem_attr(kern, dev, (int)Cfg::SMEM);
+  int per_sm = 0;
+  cudaOccupancyMaxActiveBlocksPerMultiprocessor(&per_sm, kern, Cfg::kThreads, Cfg::SMEM);
+  if (per_sm < 1) per_sm = 1;
+  kern<<<num_sms * per_sm, Cfg::kThreads, Cfg::SMEM, s>>>(kp, plans, vx, w.alias, w.tflag, w.vtab, w.y1tab, frames,
+                                                          coff, pitch, pi, icap, pvv, vcap, clip_status);
+}
+
 cudaError_t launch_team(const FKParams& kp, const vp_clip_plan* plans, int n, const ResizeWs& w, const uint8_t* frames,
                         const int64_t* coff, const int64_t* pitch, void* pi, int64_t icap, void* pvv, int64_t vcap,
-                        int32_t* clip_status, int num_sms, cudaStream_t s) {
-  const VIdx vx = ws_vidx(w, n, 4);
+                        int32_t* clip_status, int dev, int num_sms, cudaStream_t s) {
   dim3 tg((kTabInH + 127) / 128, n);
-  team_vtab_kernel<<<tg, 128, 0, s>>>(plans, vx, w.alias, w.vtab, w.y1tab, w.tflag);
-  const bool preset = kp.p == 16 && kp.m == 2 && kp.tp == 2;       // Qwen2.5/3-VL geometry: compile-time addressing
-  auto kern = kp.out_f32 ? (preset ? resize_team_kernel<kTeamUL, true, 16, 2, 2> : resize_team_kernel<kTeamUL, true, 0, 0, 0>)
-                         : (preset ? resize_team_kernel<kTeamUL, false, 16, 2, 2> : resize_team_kernel<kTeamUL, false, 0, 0, 0>);
-  int per_sm = 0;
-  cudaOccupancyMaxActiveBlocksPerMultiprocessor(&per_sm, kern, kTT, 0);
-  if (per_sm < 1) per_sm = 1;
-  kern<<<num_sms * per_sm, kTT, 0, s>>>(kp, plans, vx, w.alias, w.tflag, w.vtab, w.y1tab, frames, coff, pitch, pi, icap,
-                                        pvv, vcap, clip_status);
+  team_vtab_kernel<<<tg, 128, 0, s>>>(plans, coff, pitch, w.alias, w.vtab, w.y1tab, w.tflag);
+  const bool preset = kp.p == 16 && kp.m == 2 && kp.tp == 2;
+  if (kp.out_f32) {
+    launch_split<kTeamNV, kTeamNH, kTeamPPL, 2, true>(kp, preset, plans, ws_vidx(w, n, 4), w, frames, coff, pitch, pi, icap,
+                                            pvv, vcap, clip_status, dev, num_sms, s);
+    launch_split<kWideNV, kWideNH, kWidePPL, 1, true>(kp, preset, plans, ws_vidx(w, n, 5), w, frames, coff, pitch, pi, icap,
+                                            pvv, vcap, clip_status, dev, num_sms, s);
+  } else {
+    launch_split<kTeamNV, kTeamNH, kTeamPPL, 2, false>(kp, preset, plans, ws_vidx(w, n, 4), w, frames, coff, pitch, pi, icap,
+                                             pvv, vcap, clip_status, dev, num_sms, s);
+    launch_split<kWideNV, kWideNH, kWidePPL, 1, false>(kp, preset, plans, ws_vidx(w, n, 5), w, frames, coff, pitch, pi, icap,
+                                             pvv, vcap, clip_status, dev, num_sms, s);
+  }
   return cudaGetLastError();
 }
 
