@@ -30,7 +30,7 @@ __all__ = [
     "smart_resize_exact_floor", "grid_thw", "clip_budget", "plan_clip", "plan_batch",
     "keys_cubic", "aa_weights", "weight_matrix", "resize_frame", "resize_pixel",
     "normalize", "temporal_pad", "patchify", "patch_coords", "bf16_rne_bits", "bf16_bits_to_f64",
-    "group_timestamps", "rope_index", "process_batch", "ClipPlan",
+    "group_timestamps", "second_per_grid", "qwen25_interval", "rope_index", "process_batch", "ClipPlan",
 ]
 
 VP_OK, VP_EINVAL, VP_EMISMATCH = 0, 1, 3
@@ -376,12 +376,29 @@ def group_timestamps(idx, src_fps: float, tp: int):
 # O11 -- MRoPE position ids + strict placeholder validation (C18-C24)
 # ---------------------------------------------------------------------------
 
-def rope_index(seqs, image_grids, video_grids, merge: int, variant: int = 0, time_interval=1):
+def second_per_grid(tp: int, sampled_fps: float) -> float:
+    """Seconds spanned by one temporal grid of a video (Qwen2.5-VL, reading C19): tp / sampled fps
+    (X: HF Qwen2_5_VLProcessor, ``second_per_grid_ts = temporal_patch_size / fps``); the sampled fps is the
+    effective fps of O1 (C23)."""
+    return tp / float(sampled_fps)
+
+
+def qwen25_interval(tokens_per_second: int, second_per_grid_t: float) -> int:
+    """Temporal id step between consecutive grids of one video (QWEN25 time-scaled MRoPE, C19):
+    tokens_per_second * int(second_per_grid_t) -- int() truncates toward zero (X: HF Qwen2.5-VL
+    ``get_rope_index``: ``time_interval = tokens_per_second * int(second_per_grid_t)``; its docstring:
+    tps 25, tp 2, fps 1 -> interval 50)."""
+    return int(tokens_per_second) * int(second_per_grid_t)
+
+
+def rope_index(seqs, image_grids, video_grids, merge: int, variant: int = 0, second_per_grid_ts=None,
+               tokens_per_second: int = 0):
     """seqs: list of 1-D int arrays of token types (0 text, 1 image, 2 video), one per sequence.
     image_grids / video_grids: lists of (t, h, w) in order of appearance across the batch.
     variant 0 (QWEN3_SPLIT): each video (t,h,w) is consumed as t grids (1,h,w) (C18).
-    variant 1/2 (QWEN2 classic / QWEN25 time-scaled): temporal id p + ti*iv (C19); iv = time_interval,
-    an int or one value per video (QWEN25: tokens_per_second * int(second_per_grid_t), X: Qwen2.5-VL).
+    variant 1 (QWEN2 classic): temporal id p + ti (C19).
+    variant 2 (QWEN25 time-scaled): temporal id p + ti*iv_v, iv_v = qwen25_interval(tokens_per_second,
+    second_per_grid_ts[v]) (C19).
     Returns (ids list of int64 [3, L] arrays, deltas list, seq_status list, batch_status).
     A visual run whose length != t*(h/m)*(w/m), or with no grid left, is VP_EMISMATCH (C24, P:165);
     grids left unused at the end of the batch make batch_status VP_EMISMATCH."""
@@ -389,8 +406,8 @@ def rope_index(seqs, image_grids, video_grids, merge: int, variant: int = 0, tim
     vid = []
     for v, g in enumerate(video_grids):
         t, h, w = (int(x) for x in g)
-        iv = time_interval[v] if isinstance(time_interval, (list, tuple)) else time_interval
-        vid += [(1, h, w, 1)] * t if variant == 0 else [(t, h, w, int(iv))]
+        iv = qwen25_interval(tokens_per_second, second_per_grid_ts[v]) if variant == 2 else 1
+        vid += [(1, h, w, 1)] * t if variant == 0 else [(t, h, w, iv)]
     grids = {1: img, 2: vid}
     used = {1: 0, 2: 0}
     all_ids, deltas, status = [], [], []

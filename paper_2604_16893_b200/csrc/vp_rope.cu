@@ -341,6 +341,7 @@ rope_fill_kernel(const int8_t* __restrict__ tt, const int64_t* __restrict__ cu, 
     if (chunk_last >= 0) c_start = chunk_last;
   }
   (void)block_max;
+  __syncthreads();                                       // every thread's pass-3 s_bad write is visible to thread 0
   if (tid == 0) {
     deltas[b] = L > 0 ? (c_text + c_A) - L : 0;        // max_id + 1 - len (C21)
     status[b] = s_bad ? VP_EMISMATCH : VP_OK;

@@ -28,10 +28,8 @@ def _gpu_rope(seqs, img, vid, m, variant=0, spg=None, tps=0):
 
 
 def _compare(seqs, img, vid, m, variant=0, spg=None, tps=0):
-    iv = 1
-    if variant == 2:
-        iv = [tps * int(s) for s in spg]
-    ids, deltas, st, bst = O.rope_index(seqs, img, vid, m, variant=variant, time_interval=iv)
+    ids, deltas, st, bst = O.rope_index(seqs, img, vid, m, variant=variant, second_per_grid_ts=spg,
+                                        tokens_per_second=tps)
     pos, gd, gst = _gpu_rope(seqs, img, vid, m, variant, spg, tps)
     assert gst[:-1].tolist() == st and gst[-1] == bst
     off = 0
@@ -82,6 +80,7 @@ def test_classic_and_time_scaled_variants():
     seqs = [I.token_types([(0, 4), (2, 12), (0, 3)]), I.token_types([(0, 1), (2, 24), (0, 2), (2, 5), (0, 1)])]
     _compare(seqs, [], vid, m, variant=1)
     _compare(seqs, [], vid, m, variant=2, spg=[1.0, 2.5, 4.0], tps=25)
+    _compare(seqs, [], vid, m, variant=2, spg=[2 / 0.7, 2 / 3.0, 2.0], tps=13)   # truncation, interval 0
 
 
 def test_text_only_and_empty():

@@ -71,14 +71,55 @@ def test_text_only_is_1d_rope():
     assert np.array_equal(ids[0], np.tile(np.arange(L), (3, 1))) and deltas == [0]
 
 
-def test_classic_variant_docstring_example():
-    """HF Qwen2-VL get_rope_index docstring: llm grid 3x2x2, interval 50 ->
-    T [0,0,0,0,50,50,50,50,100,...], H [0,0,1,1,...], W [0,1,0,1,...]."""
-    ids, deltas, st, _ = O.rope_index([np.full(12, 2)], [], [(3, 4, 4)], 2, variant=1, time_interval=50)
+def test_time_scaled_variant_docstring_example():
+    """HF Qwen2.5-VL get_rope_index docstring: `interval = tokens_per_second * temporal_patch_size / fps`;
+    fps 1, tokens_per_second 25, temporal_patch_size 2 -> llm grid 3x2x2 has
+    T [0,0,0,0,50,50,50,50,100,...], H [0,0,1,1,...], W [0,1,0,1,...].  The interval comes from the oracle's
+    own chain second_per_grid(tp, fps) -> qwen25_interval, not from the test."""
+    spg = O.second_per_grid(2, 1.0)
+    assert spg == 2.0 and O.qwen25_interval(25, spg) == 50
+    ids, deltas, st, _ = O.rope_index([np.full(12, 2)], [], [(3, 4, 4)], 2, variant=2,
+                                      second_per_grid_ts=[spg], tokens_per_second=25)
     assert ids[0][0].tolist() == [0] * 4 + [50] * 4 + [100] * 4
     assert ids[0][1].tolist() == [0, 0, 1, 1] * 3
     assert ids[0][2].tolist() == [0, 1, 0, 1] * 3
-    assert deltas == [101 - 12]
+    assert deltas == [101 - 12] and st == [O.VP_OK]
+
+
+def test_classic_variant_is_unit_interval():
+    """QWEN2 classic (C19): consecutive temporal grids one id apart; equals QWEN25 with tps*int(spg) = 1."""
+    a, da, _, _ = O.rope_index([np.full(12, 2)], [], [(3, 4, 4)], 2, variant=1)
+    assert a[0][0].tolist() == [0] * 4 + [1] * 4 + [2] * 4 and da == [3 - 12]
+    b, db, _, _ = O.rope_index([np.full(12, 2)], [], [(3, 4, 4)], 2, variant=2, second_per_grid_ts=[1.9],
+                               tokens_per_second=1)
+    assert np.array_equal(a[0], b[0]) and da == db
+
+
+def test_qwen25_interval_matches_hf():
+    """Library pin of the interval rule: HF Qwen2_5_VLModel.get_rope_index called unbound on a stub whose
+    get_vision_position_ids records the time_interval it is handed (its own id formula is not used: it is
+    wrong for t > 1 in the installed version), and Qwen2_5_VLProcessor's second_per_grid_ts = tp / fps."""
+    from transformers.models.qwen2_5_vl.modeling_qwen2_5_vl import Qwen2_5_VLModel
+    seen = []
+
+    def fake_vpi(self, start, grid, tms, sms, time_interval, device=None):
+        seen.append(time_interval)
+        n = int(grid[0]) * int(grid[1]) // sms * int(grid[2]) // sms
+        return torch.zeros(3, n, dtype=torch.long)
+
+    stub = types.SimpleNamespace(config=types.SimpleNamespace(
+        vision_config=types.SimpleNamespace(spatial_merge_size=2, tokens_per_second=25)))
+    stub.get_vision_position_ids = types.MethodType(fake_vpi, stub)
+    fps_list = [1.0, 2.0, 1.5, 0.5, 3.0, 2.0 / 3.0, 0.7, 29.97]
+    spg = [2 / f for f in fps_list]
+    grids = torch.tensor([[1, 4, 4]] * len(spg))
+    types_ = []
+    for _ in spg:
+        types_ += [0, 0] + [2] * 4
+    tt = torch.tensor([types_])
+    Qwen2_5_VLModel.get_rope_index(stub, torch.zeros_like(tt), tt, None, grids, torch.tensor(spg, dtype=torch.float64))
+    assert seen == [O.qwen25_interval(25, O.second_per_grid(2, f)) for f in fps_list]
+    assert seen == [50, 25, 25, 100, 0, 75, 50, 0]        # truncation toward zero: 1.33 -> 1, 0.667 -> 0
 
 
 def test_rope_run_invariants():
