@@ -297,6 +297,39 @@ def test_cfg5_bench_launch_sampled():
     idx = torch.tensor(rows, dtype=torch.int64, device=pv.device)
     assert_pixels(pv[idx[:, 0], idx[:, 1]].cpu(), np.array(ref), "cfg5 videos")
     assert out["video_grid_thw"].cpu().tolist() == [[32, 24, 42]] * 512
+    # every one of the 49.5 M bf16 values of the first and the last clip of the launch, element by element
+    for k in (0, len(clips) - 1):
+        fr = I.frames_u8("noise", k, o.idx, 720, 1280)
+        refk = O.process_batch(op, clips[:1], [fr], plans=oplans)["pixel_values_videos"]
+        r0 = int(ph["patch_offset"][k])
+        assert_pixels(pv[r0: r0 + o.patches].cpu(), refk, f"cfg5 clip {k} (all values)")
+        del refk
+
+
+def test_cfg5_rank_shards_byte_identical():
+    """Rank-count independence (the S:150 worker-count-independence analogue for clip sharding, DESIGN.md section
+    7): the 512-clip cfg5 job run as one call and as the shards ranks of a world of 2 / 8 / 64 would run -- each
+    shard planned on its own (offsets from 0) over the same frame bytes -- gives byte-identical rows."""
+    import paper_2604_16893_b200 as vp
+    params = I.qwen3_params(max_frames=64)
+    clips = [I.clip(1800, 30.0, 720, 1280)] * 512
+    pre = vp.VisualPreprocessor(**params)
+    pl = pre.plan(clips)
+    ph = pl.plans_host
+    off, pitch, total = pre.frames_layout(pl)
+    frames = torch.empty(total, dtype=torch.uint8, device="cuda")
+    idx_host = pl.frame_indices.cpu().numpy()
+    for k in range(len(clips)):
+        n = int(ph["n_frames"][k])
+        ids = torch.from_numpy(idx_host[ph["index_offset"][k]: ph["index_offset"][k] + n].copy()).cuda()
+        vp.synth_frames(vp.VP_SYNTH_NOISE, k, ids, 720, 1280, frames[off[k]:], int(pitch[k]))
+    offd, pitd = torch.from_numpy(off).cuda(), torch.from_numpy(pitch).cuda()
+    whole = pre.run(pl, frames, offd, pitd, strict=True)["pixel_values_videos"]
+    for a, b in ((256, 264), (448, 512), (504, 512), (0, 8)):       # shards of world 64/8/64 and rank 0
+        sp = pre.plan(clips[a:b])
+        part = pre.run(sp, frames, offd[a:b], pitd[a:b], strict=True)["pixel_values_videos"]
+        r0 = int(ph["patch_offset"][a])
+        assert torch.equal(part.view(torch.int16), whole[r0: r0 + part.shape[0]].view(torch.int16)), (a, b)
 
 
 def test_determinism_three_runs():
