@@ -38,11 +38,10 @@ namespace {
 constexpr int kTDepth = VP_TEAM_DEPTH;      // staged source rows per V warp
 constexpr int kTGrp = 8;                    // rows per refill group (one mbarrier phase)
 constexpr int kTNGrp = kTDepth / kTGrp;
-constexpr int kTRowB = 400;                 // staged bytes per row slot: 384 + 16-B alignment slack
 #ifndef VP_TEAM_NR
 #define VP_TEAM_NR 4
 #endif
-constexpr int kNR = VP_TEAM_NR;             // retire slots (rows V may run ahead of H)
+constexpr int kNR = VP_TEAM_NR;             // retire slots (rows V may run ahead of H); a multiple of 4
 #ifndef VP_TEAM_HINT
 #define VP_TEAM_HINT 0      // suspend-time hint (ns) of the V<->H retire-slot waits; 0 = spin
 #endif
@@ -108,19 +107,6 @@ __device__ __forceinline__ float2& h2(float4& v, int h) { return reinterpret_cas
 // 8k+a) -- the V lanes' stores (pixels 4L+k) hit 8 distinct 16-B granules per quarter-warp.
 __device__ __forceinline__ int tpos(int x) { return (x & ~31) | ((x & 3) << 3) | ((x & 31) >> 2); }
 
-// bytes -> floats: I2F.U8 (XU pipe) or PRMT into 2^23 + b then FADD2 -2^23 (ALU + FMA pipes); both exact.
-__device__ __forceinline__ void cvt_i2f(uint32_t w, float2& lo, float2& hi) {
-  lo = make_float2((float)(w & 0xffu), (float)((w >> 8) & 0xffu));
-  hi = make_float2((float)((w >> 16) & 0xffu), (float)(w >> 24));
-}
-__device__ __forceinline__ void cvt_magic(uint32_t w, float2& lo, float2& hi) {
-  const float2 mm = make_float2(-8388608.f, -8388608.f);
-  lo = __fadd2_rn(make_float2(__uint_as_float(__byte_perm(w, 0x4B000000u, 0x7540u)),
-                              __uint_as_float(__byte_perm(w, 0x4B000000u, 0x7541u))), mm);
-  hi = __fadd2_rn(make_float2(__uint_as_float(__byte_perm(w, 0x4B000000u, 0x7542u)),
-                              __uint_as_float(__byte_perm(w, 0x4B000000u, 0x7543u))), mm);
-}
-
 // A lane's 12 staged bytes (R0 G0 B0 R1 | G1 B1 R2 G2 | B2 R3 G3 B3 in words n0, n1, n2) as the six FFMA2 operand
 // pairs of the ring, ordered so that the accumulator quads are (R0 G0 B0 R3), (R1 G1 B1 G3), (R2 G2 B2 B3): pixels
 // 0..2 retire as whole quads (their .w is pixel 3's channel, ignored by the horizontal pass) and pixel 3 is the .w
@@ -155,13 +141,15 @@ __device__ __forceinline__ void ring4(float4 (&acc)[4][3], const float4 w, const
 // normalise (O6) as FFMA2 over the column pair, clamp (C12) in the output domain (clamp(v,0,255)*s+b ==
 // clamp(v*s+b, lo, hi) with lo/hi the images of 0 and 255, ordered), round (O9) and store the pair into every
 // temporal slot the frame fills (O7); for bf16 RNE is monotone, so clamping the rounded pair is bit-identical.
-template <bool kF32>
+template <bool kF32, bool kFold>
 __device__ __forceinline__ void store_pair(const FKParams& kp, char* q, float2 ar, float2 ag, float2 ab, int cstride,
                                            int nslots, int ti0, int tp, int p, int64_t group_stride) {
   constexpr int kEsz = kF32 ? 4 : 2;
-  const float2 n[3] = {__ffma2_rn(ar, make_float2(kp.scale[0], kp.scale[0]), make_float2(kp.bias[0], kp.bias[0])),
-                       __ffma2_rn(ag, make_float2(kp.scale[1], kp.scale[1]), make_float2(kp.bias[1], kp.bias[1])),
-                       __ffma2_rn(ab, make_float2(kp.scale[2], kp.scale[2]), make_float2(kp.bias[2], kp.bias[2]))};
+  // kFold: the pair weights carry the (channel-uniform) scale and the accumulators start at the bias, so the sums
+  // are already normalised
+  const float2 n[3] = {kFold ? ar : __ffma2_rn(ar, make_float2(kp.scale[0], kp.scale[0]), make_float2(kp.bias[0], kp.bias[0])),
+                       kFold ? ag : __ffma2_rn(ag, make_float2(kp.scale[1], kp.scale[1]), make_float2(kp.bias[1], kp.bias[1])),
+                       kFold ? ab : __ffma2_rn(ab, make_float2(kp.scale[2], kp.scale[2]), make_float2(kp.bias[2], kp.bias[2]))};
   uint2 o[3];                                      // per channel: the pair as float2 (f32) or bf16x2 in .x (bf16)
 #pragma unroll
   for (int c = 0; c < 3; ++c) {
@@ -189,7 +177,7 @@ __device__ __forceinline__ void store_pair(const FKParams& kp, char* q, float2 a
   }
 }
 
-template <int NV, int NH, int PPL, int kUL, bool kF32, int P, int M, int TP, int MINB>
+template <int NV, int NH, int PPL, int kUL, bool kF32, bool kFold, int P, int M, int TP, int MINB>
 __global__ void __launch_bounds__((NV + NH) * 32, MINB)
 resize_split_kernel(FKParams kp, const vp_clip_plan* __restrict__ plans, const VIdx vx, const int* __restrict__ tab_alias,
                     const int* __restrict__ tab_flag, const float4* __restrict__ vtab, const int* __restrict__ y1tab,
@@ -201,7 +189,7 @@ resize_split_kernel(FKParams kp, const vp_clip_plan* __restrict__ plans, const V
   constexpr int kRowB = Cfg::kRowB;
   // preset geometry (p % 4 == 0 and p*m % 4 == 0): every out_h is a multiple of 4, so with 4 retire slots the slot of
   // output row i is i % 4 = the static unroll index U
-  constexpr bool kStatic = P > 0 && (P % 4) == 0 && ((P * M) % 4) == 0 && kNR == 4;
+  constexpr bool kStatic = P > 0 && (P % 4) == 0 && ((P * M) % 4) == 0 && (kNR % 4) == 0;
   extern __shared__ __align__(128) unsigned char smem[];
   const int tid = threadIdx.x;
   const int warp = __shfl_sync(0xffffffffu, tid >> 5, 0);
@@ -338,7 +326,7 @@ resize_split_kernel(FKParams kp, const vp_clip_plan* __restrict__ plans, const V
       }
 #define VP_V_RETIRE(U)                                                                                       \
       {                                                                                                       \
-        const uint32_t rs = kStatic ? (uint32_t)U : rr % kNR;                                                 \
+        const uint32_t rs = kStatic ? sbase + (uint32_t)U : rr % kNR;                                                 \
         mbar_wait_uni<VP_TEAM_HINT>(&rempty[rs], ((rr / kNR) & 1) ^ 1);                                       \
         const uint32_t ra = vsa + rs * kSlotB;                                                                \
         const float4* a = acc[U];                     /* pixels 0..2 are quads .xyz; pixel 3 is the .w column */ \
@@ -354,6 +342,7 @@ resize_split_kernel(FKParams kp, const vp_clip_plan* __restrict__ plans, const V
       int4 ye_next = __ldg(reinterpret_cast<const int4*>(y1));
       for (int ib = 0; ib < out_h; ib += 4) {
         const int4 ye = ye_next;                  // window ends of rows ib..ib+3, prefetched one group ahead
+        const uint32_t sbase = kNR == 4 ? 0u : ((rr >> 2) % (uint32_t)(kNR / 4)) * 4u;   // retire slots of this group
         if (ib + 4 < out_h) ye_next = __ldg(reinterpret_cast<const int4*>(y1 + ib + 4));
 #define VP_V_ROW(U, YE)                                                                                      \
         if (kStatic || ib + U < out_h) {                                                                      \
@@ -420,7 +409,7 @@ resize_split_kernel(FKParams kp, const vp_clip_plan* __restrict__ plans, const V
           const int x = xu + u;
           const float wa = (x >= w0.x0 && x < w0.x1) ? (float)(keys_d(((double)x - w0.c + 0.5) * w0.inv) / r0) : 0.f;
           const float wb = (x >= w1.x0 && x < w1.x1) ? (float)(keys_d(((double)x - w1.c + 0.5) * w1.inv) / r1) : 0.f;
-          wp[pp][u] = make_float2(wa, wb);
+          wp[pp][u] = kFold ? make_float2(wa * kp.scale[0], wb * kp.scale[0]) : make_float2(wa, wb);
           toff[pp][u] = buf_s + (uint32_t)tpos(min(x - pa, kPx - 1)) * 16u;   // slack taps (weight 0) stay in the row
         }
         const int jl0 = ja % B, wbk = ja / B, mw = jl0 / p, px = jl0 - mw * p;
@@ -442,11 +431,18 @@ resize_split_kernel(FKParams kp, const vp_clip_plan* __restrict__ plans, const V
     bool hst[PPL];
 #pragma unroll
     for (int pp = 0; pp < PPL; ++pp) hst[pp] = writable && hact[pp];
-    auto hrow = [&](uint32_t so, int ro) {          // H of one retired row in slot offset so, output row offset ro
+    auto hrow = [&](uint32_t so, char* const (&qb)[PPL]) {   // H of one retired row in slot offset so
 #pragma unroll
       for (int pp = 0; pp < PPL; ++pp) {
         if (hst[pp]) {
-          float2 ar = make_float2(0.f, 0.f), ag = ar, ab = ar;
+          float2 ar, ag, ab;
+          if (kFold) {
+            ar = make_float2(kp.bias[0], kp.bias[0]);
+            ag = make_float2(kp.bias[1], kp.bias[1]);
+            ab = make_float2(kp.bias[2], kp.bias[2]);
+          } else {
+            ar = ag = ab = make_float2(0.f, 0.f);
+          }
 #pragma unroll
           for (int u = 0; u < kUL; ++u) {
             const float4 v = lds_f4(toff[pp][u] + so);
@@ -454,8 +450,7 @@ resize_split_kernel(FKParams kp, const vp_clip_plan* __restrict__ plans, const V
             ag = __ffma2_rn(make_float2(v.y, v.y), wp[pp][u], ag);
             ab = __ffma2_rn(make_float2(v.z, v.z), wp[pp][u], ab);
           }
-          store_pair<kF32>(kp, fbase + (int64_t)(ro + colpart[pp]) * kEsz, ar, ag, ab, cstride, nslots, ti0, tp, p,
-                           group_stride);
+          store_pair<kF32, kFold>(kp, qb[pp], ar, ag, ab, cstride, nslots, ti0, tp, p, group_stride);
         }
       }
     };
@@ -465,12 +460,19 @@ resize_split_kernel(FKParams kp, const vp_clip_plan* __restrict__ plans, const V
         // of a group share i / p
         const int ro_grp = (ib / B) * hb_stride + ((ib / p) % m) * m * D + (ib % p) * p;
         const uint32_t par = (rr / kNR) & 1;
+        const uint32_t sbase = kNR == 4 ? 0u : ((rr >> 2) % (uint32_t)(kNR / 4)) * 4u;
+        char* gb[PPL];                              // output address of row ib, per column pair
+#pragma unroll
+        for (int pp = 0; pp < PPL; ++pp) gb[pp] = fbase + (int64_t)(ro_grp + colpart[pp]) * kEsz;
 #pragma unroll
         for (int U = 0; U < 4; ++U) {
-          mbar_wait_uni<VP_TEAM_HINT>(&rfull[U], par);
-          hrow((uint32_t)U * kSlotB, ro_grp + U * p);
+          char* qb[PPL];
+#pragma unroll
+          for (int pp = 0; pp < PPL; ++pp) qb[pp] = gb[pp] + U * p * kEsz;   // rows ib..ib+3 share i / p
+          mbar_wait_uni<VP_TEAM_HINT>(&rfull[sbase + U], par);
+          hrow((sbase + (uint32_t)U) * kSlotB, qb);
           __syncwarp();
-          mbar_arrive_if(&rempty[U], l0);
+          mbar_arrive_if(&rempty[sbase + U], l0);
         }
         rr += 4;
       }
@@ -478,7 +480,11 @@ resize_split_kernel(FKParams kp, const vp_clip_plan* __restrict__ plans, const V
       for (int i = 0; i < out_h; ++i) {
         const uint32_t rs = rr % kNR;
         mbar_wait_uni<VP_TEAM_HINT>(&rfull[rs], (rr / kNR) & 1);
-        hrow(rs * kSlotB, (i / B) * hb_stride + ((i / p) % m) * m * D + (i % p) * p);
+        char* qb[PPL];
+#pragma unroll
+        for (int pp = 0; pp < PPL; ++pp)
+          qb[pp] = fbase + (int64_t)((i / B) * hb_stride + ((i / p) % m) * m * D + (i % p) * p + colpart[pp]) * kEsz;
+        hrow(rs * kSlotB, qb);
         __syncwarp();
         mbar_arrive_if(&rempty[rs], l0);
         ++rr;
@@ -715,8 +721,11 @@ void launch_split(const FKParams& kp, bool preset, const vp_clip_plan* plans, co
                   int64_t vcap, int32_t* clip_status, int dev, int num_sms, cudaStream_t s) {
   using Cfg = SplitCfg<NV, NH>;
   // Qwen2.5/3-VL geometry (p16 m2 tp2) with compile-time output addressing, else runtime parameters
-  auto kern = preset ? resize_split_kernel<NV, NH, PPL, kTeamUL, kF32, 16, 2, 2, MINB>
-                     : resize_split_kernel<NV, NH, PPL, kTeamUL, kF32, 0, 0, 0, MINB>;
+  // a channel-uniform scale (e.g. Qwen mean = std = 0.5) folds into the horizontal weights (store_pair)
+  const bool fold = kp.scale[0] == kp.scale[1] && kp.scale[1] == kp.scale[2];
+  auto kern = preset ? (fold ? resize_split_kernel<NV, NH, PPL, kTeamUL, kF32, true, 16, 2, 2, MINB>
+                             : resize_split_kernel<NV, NH, PPL, kTeamUL, kF32, false, 16, 2, 2, MINB>)
+                     : resize_split_kernel<NV, NH, PPL, kTeamUL, kF32, false, 0, 0, 0, MINB>;
   set_smem_attr(kern, dev, (int)Cfg::SMEM);
   int per_sm = 0;
   cudaOccupancyMaxActiveBlocksPerMultiprocessor(&per_sm, kern, Cfg::kThreads, Cfg::SMEM);
