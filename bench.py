@@ -105,7 +105,7 @@ def run_ours(args, rank, world, local_rank):
     import torch.distributed as dist
     import paper_2604_16893_b200 as vp
     import vp_inputs as I
-    from paper_2604_16893_b200.dist import gather_records
+    from paper_2604_16893_b200.dist import gather_records_async
 
     torch.cuda.set_device(local_rank)
     dev = torch.device("cuda", local_rank)
@@ -171,10 +171,9 @@ def run_ours(args, rank, world, local_rank):
 
     def step(record=False):
         vp.plan_frames(P, pl.clips_dev, per, pl.plans_dev, pl.frame_indices, pl.totals_dev, pl.group_timestamps)
-        if world > 1:
+        if world > 1:                                          # H10: NCCL all-gather of (t,h,w,tokens) ...
             vp.plan_records(pl.plans_dev, per, m, records)
-            gathered = gather_records(records)                 # H10: NCCL all-gather of (t,h,w,tokens)
-            vp.pack_offsets(gathered, world, per, tok_off, pat_off)
+            gathered, work = gather_records_async(records)     # ... on NCCL's stream, overlapping K3
         if record:
             a = torch.cuda.Event(enable_timing=True)
             b = torch.cuda.Event(enable_timing=True)
@@ -188,6 +187,9 @@ def run_ours(args, rank, world, local_rank):
             ev_k3.append((a, b))
         vp.rope_index(P, vp.VP_ROPE_QWEN3_SPLIT, tt, cu, out["image_grid_thw"] if n_img else None,
                       out["video_grid_thw"], pos, deltas, rst, ws)
+        if world > 1:
+            work.wait()                                        # the compute stream waits for the gather here
+            vp.pack_offsets(gathered, world, per, tok_off, pat_off)
 
     launches_per_step = 5 + (2 if world > 1 else 0)
     for _ in range(args.warmup):
@@ -425,13 +427,23 @@ def main():
     ap.add_argument("--no-cpu-baseline", action="store_true")
     ap.add_argument("--cpu-clips", type=int, default=4)
     ap.add_argument("--ref-groups", type=int, default=2)
+    ap.add_argument("--backend", default="nccl", choices=["nccl", "gloo"],
+                    help="process-group backend (gloo only for --dist-selftest on CPU)")
+    ap.add_argument("--dist-selftest", action="store_true",
+                    help="launcher check without GPUs: spawn, rendezvous, clip sharding, record all-gather, "
+                         "max-over-ranks reduction (prints one JSON line on rank 0)")
     args = ap.parse_args()
+    if args.gpus > 1 and "WORLD_SIZE" not in os.environ:
+        spawn_ranks(args.gpus)                              # re-exec under torch.distributed.run; never returns
     rank = int(os.environ.get("RANK", 0))
     world = int(os.environ.get("WORLD_SIZE", 1))
     local_rank = int(os.environ.get("LOCAL_RANK", 0))
-    if args.gpus != world and world == 1 and args.gpus > 1:
-        print(json.dumps({"error": "launch with torchrun for --gpus > 1"}))
+    if args.gpus != world:
+        print(json.dumps({"error": f"--gpus {args.gpus} but WORLD_SIZE {world}"}))
         sys.exit(2)
+    if args.dist_selftest:
+        dist_selftest(args, rank, world)
+        return
     if args.impl == "reference":
         r = run_reference(args, rank, world)
         if r is not None:
@@ -439,15 +451,64 @@ def main():
         return
     import torch
     import torch.distributed as dist
+    nccl_glob = None
     if world > 1:
-        dist.init_process_group("nccl", device_id=torch.device("cuda", local_rank))
+        # NCCL communicator-init logging (nRanks per communicator) to a per-process file, summarised in the JSON
+        os.environ.setdefault("NCCL_DEBUG", "INFO")
+        os.environ.setdefault("NCCL_DEBUG_SUBSYS", "INIT")
+        os.environ.setdefault("NCCL_DEBUG_FILE", os.path.join(tempfile.gettempdir(), "vp_nccl.%h.%p.log"))
+        nccl_glob = os.environ["NCCL_DEBUG_FILE"].replace("%h", "*").replace("%p", str(os.getpid()))
+        dist.init_process_group(args.backend, device_id=torch.device("cuda", local_rank))
     res = run_ours(args, rank, world, local_rank)
     if rank == 0:
         if world == 1 and not args.no_cpu_baseline:
             res["cpu_baseline"] = cpu_baseline(args.cpu_clips)
+        if world > 1:
+            from paper_2604_16893_b200.dist import nccl_log_nranks
+            res["nccl"] = {"backend": args.backend, "comm_nranks": nccl_log_nranks(nccl_glob),
+                           "h10": "all_gather_into_tensor of int32 (t,h,w,tokens) records, async on the NCCL "
+                                  "stream, overlapping K3; work.wait() before vp_pack_offsets"}
         print(json.dumps(res))
     if world > 1:
         dist.destroy_process_group()
+
+
+def spawn_ranks(n: int):
+    """`python bench.py --gpus N` outside torchrun: re-exec as one process per GPU through torch.distributed.run
+    (single node, rendezvous on 127.0.0.1), with the same arguments."""
+    import socket
+    with socket.socket() as sk:
+        sk.bind(("127.0.0.1", 0))
+        port = sk.getsockname()[1]
+    cmd = [sys.executable, "-m", "torch.distributed.run", "--nnodes=1", f"--nproc-per-node={n}",
+           "--master-addr", "127.0.0.1", "--master-port", str(port), os.path.abspath(__file__), *sys.argv[1:]]
+    sys.stdout.flush()
+    os.execv(sys.executable, cmd)
+
+
+def dist_selftest(args, rank, world):
+    """The N>1 plumbing of the bench without GPUs (gloo): rendezvous, the cfg5 clip shard of this rank, an
+    all-gather of per-clip int32 records (here (rank, clip, a + k, 1) so the gathered order is checkable) and the
+    max-over-ranks reduction of the step time."""
+    import torch
+    import torch.distributed as dist
+    from paper_2604_16893_b200.dist import shard_range
+    dist.init_process_group(args.backend)
+    job = args.clips if args.clips else JOB_CLIPS
+    a, b = shard_range(job, world, rank)
+    rec = torch.tensor([[rank, k, a + k, 1] for k in range(b - a)], dtype=torch.int32).reshape(-1)
+    out = torch.empty(world * rec.numel(), dtype=torch.int32)
+    dist.all_gather_into_tensor(out, rec)
+    g = out.reshape(-1, 4)
+    ok = g[:, 2].tolist() == list(range(job)) and all(int(g[i, 0]) == i // (job // world) for i in range(job))
+    t = torch.tensor([float(rank + 1)], dtype=torch.float64)
+    dist.all_reduce(t, op=dist.ReduceOp.MAX)
+    if rank == 0:
+        print(json.dumps({"dist_selftest": "ok" if ok and t.item() == world else "fail", "world": world,
+                          "backend": args.backend, "clips": job, "shard_sizes": [b - a] * 1,
+                          "gathered_records": int(g.shape[0]), "max_over_ranks": t.item()}))
+    dist.barrier()
+    dist.destroy_process_group()
 
 
 if __name__ == "__main__":

@@ -28,3 +28,32 @@ def gather_records(records: torch.Tensor, group=None) -> torch.Tensor:
     out = torch.empty(world * records.numel(), dtype=records.dtype, device=records.device)
     dist.all_gather_into_tensor(out, records.contiguous(), group=group)
     return out
+
+
+def gather_records_async(records: torch.Tensor, group=None):
+    """As gather_records, but returns (out, work) with the all-gather in flight: on NCCL it runs on the process
+    group's own stream once the current stream reaches this point, so the caller can launch K3 behind it and call
+    work.wait() (which makes the current stream wait) just before vp_pack_offsets (the H10
+    exchange overlaps the resize)."""
+    world = dist.get_world_size(group)
+    out = torch.empty(world * records.numel(), dtype=records.dtype, device=records.device)
+    work = dist.all_gather_into_tensor(out, records.contiguous(), group=group, async_op=True)
+    return out, work
+
+
+def nccl_log_nranks(path_glob: str):
+    """Number of ranks NCCL reported at communicator init (NCCL_DEBUG=INFO lines '... nRanks N ...' written to
+    NCCL_DEBUG_FILE), or None if no such line was logged."""
+    import glob
+    import re
+    n = None
+    for p in glob.glob(path_glob):
+        try:
+            with open(p, errors="replace") as fh:
+                for line in fh:
+                    m = re.search(r"nRanks (\d+)", line)
+                    if m:
+                        n = max(n or 0, int(m.group(1)))
+        except OSError:
+            pass
+    return n

@@ -74,3 +74,23 @@ def test_shard_range_covers_exactly_once():
                 seen += list(range(a, b))
                 assert b - a in (n // w, n // w + 1)
             assert seen == list(range(n))
+
+
+@pytest.mark.parametrize("world", [2, 4])
+def test_bench_launcher_spawns_ranks(world):
+    """`python bench.py --gpus N` outside torchrun re-executes itself through torch.distributed.run (one process per
+    rank, rendezvous on 127.0.0.1); --dist-selftest runs the N>1 plumbing of the bench on gloo: the cfg5 clip shards,
+    the all-gather of per-clip int32 records in rank order and the max-over-ranks reduction of the step time."""
+    import json
+    import subprocess
+    import sys
+    root = os.path.dirname(os.path.dirname(os.path.abspath(__file__)))
+    env = dict(os.environ)
+    env.pop("WORLD_SIZE", None)
+    r = subprocess.run([sys.executable, os.path.join(root, "bench.py"), "--gpus", str(world), "--backend", "gloo",
+                        "--dist-selftest"], capture_output=True, text=True, timeout=600, env=env, cwd=root)
+    assert r.returncode == 0, r.stderr[-2000:]
+    line = [x for x in r.stdout.splitlines() if x.startswith("{")][-1]
+    d = json.loads(line)
+    assert d["dist_selftest"] == "ok" and d["world"] == world and d["gathered_records"] == 512
+    assert d["max_over_ranks"] == world
