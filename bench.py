@@ -121,11 +121,11 @@ def run_ours(args, rank, world, local_rank):
     clips = all_clips[a:b]
     per = len(clips)
     pre = vp.VisualPreprocessor(device=dev, **params)
-    P = pre.params
-    m = P.merge_size
+    m = pre.params.merge_size
 
     # ---------------- setup (untimed) ----------------
     pl = pre.plan(clips)
+    P = pre.launch_params(pl)              # params + the plan's kernel-variant launch hint
     ph = pl.plans_host
     off, pitch, total_bytes = pre.frames_layout(pl)
     frames = torch.empty(total_bytes, dtype=torch.uint8, device=dev)
@@ -274,7 +274,7 @@ def run_e2e(args, pre, pl, frames, off, pitch, out, tt, cu, pos, deltas, rst, ws
     import torch.distributed as dist
     import paper_2604_16893_b200 as vp
 
-    P = pre.params
+    P = pre.launch_params(pl)
     chunk = max(1, min(args.e2e_chunk, per))
     ring = max(chunk, min(2 * chunk, per))
     clip_bytes = int(off[1] - off[0]) if per > 1 else int(frames.numel())

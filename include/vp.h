@@ -43,7 +43,7 @@ typedef enum {
   VP_EMISMATCH = 3,  /* placeholder run length != t*h*w/m^2, or grids left over */
   VP_ECAPACITY = 4,  /* an output buffer is smaller than the plan requires */
   VP_ECUDA = 5,      /* kernel launch failed */
-  VP_EUNSUPPORTED = 6 /* a resize ratio beyond the kernels' shared-memory envelope (>~250x) */
+  VP_EUNSUPPORTED = 6 /* a configuration beyond the kernels' envelope (merge_size*patch_size > 64) */
 } vp_status;
 
 typedef enum { VP_SAMPLE_CENTER_BIN = 0 /* S:78 (C1, C2) */ } vp_sampling;
@@ -70,7 +70,10 @@ typedef struct {
   double  mean[3];             /* per-channel mean (C13), 0.5 for Qwen3-VL */
   double  std[3];              /* per-channel std (C13), 0.5 for Qwen3-VL */
   int32_t out_dtype;           /* vp_dtype of pixel_values */
-  int32_t reserved_;
+  int32_t launch_mask;         /* optional launch hint for vp_resize_normalize_patchify: totals[VP_TOT_VARIANTS]
+                                  of the plan (bit v = some valid clip uses kernel variant v); kernels of absent
+                                  variants are not launched.  0 = unknown: launch every kernel.  Ignored by the
+                                  other calls.  A mask missing a present variant leaves its clips unwritten. */
 } vp_params;                   /* 112 bytes */
 
 /* One input clip (S:42-47 VideoMetadata source fields).  Images: is_image=1, the frame count and
@@ -117,6 +120,7 @@ enum {
   VP_TOT_TILES = 8,      /* private */
   VP_TOT_FLAGS = 9,      /* bit0 frame_indices overflow, bit1 timestamps overflow */
   VP_TOT_N_INVALID = 10, /* clips with status != VP_OK */
+  VP_TOT_VARIANTS = 11,  /* bitmask of the kernel variants of the valid clips (the vp_params.launch_mask hint) */
   VP_TOT_LEN = 12
 };
 
@@ -166,8 +170,9 @@ vp_status vp_plan_frames(const vp_params* p, const vp_clip_desc* clips, int32_t 
  *   pixel_values_videos (dev, nullable if no videos) [vid_rows_cap, 3*tp*p*p] of out_dtype
  *   image_grid_thw, video_grid_thw (dev) [n_images,3] / [n_videos,3] int64 (HF convention)
  *   clip_status (dev, nullable) [n] int32 output: VP_OK, VP_EINVAL (invalid plan), VP_ECAPACITY
- *                      (rows beyond the cap; that clip's rows are not written) or VP_EUNSUPPORTED
- *                      (a per-axis downscale beyond ~34x; that clip's rows are not written)
+ *                      (rows beyond the cap; that clip's rows are not written).  Every resize ratio is
+ *                      supported (downscales beyond the shared-memory window tables, ~34x per axis, take a
+ *                      direct f64 kernel)
  *   workspace (dev)    vp_resize_workspace_bytes(n) bytes, 256-B aligned, caller-owned scratch (work index and
  *                      per-clip weight tables, rebuilt on every call; contents need not persist)
  * Errors: VP_EINVAL (incl. a missing / short / misaligned workspace), VP_EUNSUPPORTED, VP_ECUDA.

@@ -212,6 +212,13 @@ class VisualPreprocessor:
                 cur += int(ph["n_frames"][k]) * int(ph["in_h"][k]) * int(pitch[k])
         return off, pitch, cur
 
+    def launch_params(self, pl: Plan) -> VpParams:
+        """self.params with the plan's kernel-variant mask as the launch hint (vp_params.launch_mask)."""
+        p = VpParams()
+        C.pointer(p)[0] = self.params
+        p.launch_mask = int(pl.totals["variants"]) if pl.totals is not None else 0
+        return p
+
     def alloc_outputs(self, pl: Plan):
         dt = torch.float32 if self.params.out_dtype == VP_OUT_F32 else torch.bfloat16
         t = pl.totals
@@ -230,7 +237,8 @@ class VisualPreprocessor:
         VP_EUNSUPPORTED) raises.  Clips with invalid descriptors are recorded as VP_EINVAL in
         ``clip_status`` / the plan without aborting the batch."""
         out = self.alloc_outputs(pl) if out is None else out
-        resize_normalize_patchify(self.params, pl.plans_dev, pl.n, frames, clip_byte_offset,
+        params = self.launch_params(pl)
+        resize_normalize_patchify(params, pl.plans_dev, pl.n, frames, clip_byte_offset,
                                   row_pitch, out["pixel_values"] if out["pixel_values"].numel() else None,
                                   out["pixel_values_videos"] if out["pixel_values_videos"].numel() else None,
                                   out["image_grid_thw"], out["video_grid_thw"], out["clip_status"],

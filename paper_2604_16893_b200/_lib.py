@@ -21,7 +21,7 @@ VP_SYNTH_RAMP, VP_SYNTH_NOISE = 0, 1
 
 # totals[] indices (vp.h)
 TOT = dict(indices=0, img_rows=1, vid_rows=2, img_tokens=3, vid_tokens=4, n_images=5, n_videos=6,
-           vid_groups=7, tiles=8, flags=9, n_invalid=10)
+           vid_groups=7, tiles=8, flags=9, n_invalid=10, variants=11)
 TOT_LEN = 12
 
 EXPORTED = ["vp_plan_frames", "vp_resize_workspace_bytes", "vp_resize_normalize_patchify", "vp_rope_index_workspace_bytes", "vp_rope_index",
@@ -34,7 +34,7 @@ class VpParams(C.Structure):
                 ("patch_size", C.c_int32), ("merge_size", C.c_int32), ("video_max_pixels", C.c_int64),
                 ("image_max_pixels", C.c_int64), ("min_pixels", C.c_int64), ("budget_mode", C.c_int32),
                 ("sampling", C.c_int32), ("mean", C.c_double * 3), ("std", C.c_double * 3),
-                ("out_dtype", C.c_int32), ("reserved_", C.c_int32)]
+                ("out_dtype", C.c_int32), ("launch_mask", C.c_int32)]
 
 
 DESC_DTYPE = np.dtype([("total_source_frames", "<i8"), ("source_fps", "<f8"), ("height", "<i4"),

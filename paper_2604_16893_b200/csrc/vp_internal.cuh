@@ -50,7 +50,8 @@ constexpr int kTotLen = VP_TOT_LEN;
 // KV_GENERIC covers everything else (vp_resize.cu, token tiles).  A clip's items (tile_count)
 // are n_frames x n_strips for the fast variants, 0 for generic.  Integer / f64 exact.
 // ------------------------------------------------------------------------------------------
-enum { KV_MILD = 0, KV_MEDIUM = 1, KV_STRONG = 2, KV_GENERIC = 3, KV_COPY = 4, KV_TEAM = 5, KV_WIDE = 6 };
+enum { KV_MILD = 0, KV_MEDIUM = 1, KV_STRONG = 2, KV_GENERIC = 3, KV_COPY = 4, KV_TEAM = 5, KV_WIDE = 6, KV_DIRECT = 7 };
+constexpr int kGenericMaxTaps = 140;  // window-table length of the generic kernel (vp_resize.cu): ~34x per axis
 constexpr int kRing = 5;          // vertical ring slots: max live output rows per source row for in/out > 0.8
 constexpr int kInHMax = 1088;     // source rows supported by the fast kernel's per-row weight table
 constexpr int kWListMax = 6144;   // vertical weights (sum of window lengths) held in smem
@@ -148,6 +149,14 @@ __host__ __device__ __forceinline__ int pair_union_bound(int in, int out) {
   return (int)floor(s + 4.0 * fs + 1.0 + 1e-9);
 }
 
+// KV_GENERIC, or KV_DIRECT when a window exceeds the generic kernel's weight tables (4*max(in/out,1) + 2 taps
+// > kGenericMaxTaps): those clips take the direct f64 kernel (vp_resize.cu), so every ratio is supported (C9).
+__host__ __device__ __forceinline__ int generic_or_direct(int in_h, int in_w, int out_h, int out_w) {
+  const double fv = (double)in_h / out_h, fh = (double)in_w / out_w;
+  const double fs = fmax(fmax(fv, fh), 1.0);
+  return 4.0 * fs + 2.0 > (double)kGenericMaxTaps ? KV_DIRECT : KV_GENERIC;
+}
+
 __host__ __device__ __forceinline__ int select_variant(int in_h, int in_w, int out_h, int out_w, int p) {
   if (in_h == out_h && in_w == out_w && (p & 1) == 0) return KV_COPY;
   if (in_h >= out_h && in_w >= out_w && (p & 1) == 0 && in_h <= kTabInH && out_h <= kTabOutH &&
@@ -160,13 +169,13 @@ __host__ __device__ __forceinline__ int select_variant(int in_h, int in_w, int o
   // live output rows per source row <= floor(4/s)+1 for upscale (<= 5 iff s > 0.8) and <= 5 for downscale
   // (trimmed windows; brute-forced in tests/test_oracle_pixels.py::test_live_rows_bound).  The streaming kernel
   // stores column pairs (bf16x2 / float2), so it needs an even patch size.
-  if ((p & 1) || !(sv > 0.8) || in_h > kInHMax || out_h > kOutHMax) return KV_GENERIC;
+  if ((p & 1) || !(sv > 0.8) || in_h > kInHMax || out_h > kOutHMax) return generic_or_direct(in_h, in_w, out_h, out_w);
   const double sh = (double)in_w / (double)out_w;
-  if (sh < 0.6 || fast_strip_width(in_w, out_w) < 16) return KV_GENERIC;
+  if (sh < 0.6 || fast_strip_width(in_w, out_w) < 16) return generic_or_direct(in_h, in_w, out_h, out_w);
   const int th = axis_max_taps(in_w, out_w);
   for (int v = KV_MILD; v <= KV_STRONG; ++v)
     if (th <= fast_lhm(v)) return v;
-  return KV_GENERIC;
+  return generic_or_direct(in_h, in_w, out_h, out_w);
 }
 
 }  // namespace vp

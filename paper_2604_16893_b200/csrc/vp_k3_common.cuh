@@ -197,10 +197,11 @@ cudaError_t launch_index(const vp_clip_plan* plans, int n, const int64_t* coff, 
                          const ResizeWs& w, cudaStream_t s);
 cudaError_t launch_team(const FKParams& kp, const vp_clip_plan* plans, int n, const ResizeWs& w, const uint8_t* frames,
                         const int64_t* coff, const int64_t* pitch, void* pi, int64_t icap, void* pvv, int64_t vcap,
-                        int32_t* clip_status, int dev, int num_sms, cudaStream_t s);
+                        int32_t* clip_status, int dev, int num_sms, unsigned mask, cudaStream_t s);
 cudaError_t launch_fast_variants(const FKParams& kp, const vp_clip_plan* plans, int n, const ResizeWs& w,
                                  const uint8_t* frames, const int64_t* coff, const int64_t* pitch, void* pi,
-                                 int64_t icap, void* pvv, int64_t vcap, int dev, int num_sms, cudaStream_t s);
+                                 int64_t icap, void* pvv, int64_t vcap, int dev, int num_sms, unsigned mask,
+                                 cudaStream_t s);
 FKParams make_fkparams(const vp_params* p);
 
 }  // namespace vp

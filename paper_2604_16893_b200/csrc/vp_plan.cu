@@ -100,7 +100,9 @@ plan_kernel(vp_params P, const vp_clip_desc* __restrict__ clips, int n, vp_clip_
             int64_t* __restrict__ totals) {
   __shared__ int64_t warp_tot[32][kNScan];
   __shared__ int64_t carry[kNScan];
+  __shared__ int s_variants;                      // VP_TOT_VARIANTS: OR of 1 << kernel_variant over valid clips
   const int tid = threadIdx.x, lane = tid & 31, warp = tid >> 5;
+  if (tid == 0) s_variants = 0;
   const int64_t m2 = (int64_t)P.merge_size * P.merge_size;
   if (tid < kNScan) carry[tid] = 0;
   __syncthreads();
@@ -121,6 +123,7 @@ plan_kernel(vp_params P, const vp_clip_desc* __restrict__ clips, int n, vp_clip_
       v[S_GROUPS] = r.is_image ? 0 : r.gt;
       const int kv = select_variant(clips[k].height, clips[k].width, r.out_h, r.out_w, P.patch_size);
       r.variant = kv;
+      atomicOr(&s_variants, 1 << kv);
       if (kv == KV_COPY) {
         v[S_TILES] = (int64_t)r.n * (r.gh / P.merge_size) * copy_wchunks(r.gw, P.merge_size);
       } else if (kv == KV_TEAM || kv == KV_WIDE) {
@@ -208,7 +211,7 @@ plan_kernel(vp_params P, const vp_clip_desc* __restrict__ clips, int n, vp_clip_
     totals[VP_TOT_TILES] = carry[S_TILES];
     totals[VP_TOT_FLAGS] = 0;                     // plan_fill_kernel ORs overflow bits in
     totals[VP_TOT_N_INVALID] = carry[S_INVALID];
-    totals[11] = 0;
+    totals[VP_TOT_VARIANTS] = s_variants;
   }
 }
 

@@ -21,7 +21,7 @@ namespace vp {
 namespace {
 
 constexpr int kThreads = 256;
-constexpr int kMaxTaps = 140;          // window length bound: supports downscale up to ~34x per axis
+constexpr int kMaxTaps = kGenericMaxTaps;   // window length bound (~34x per axis); larger: KV_DIRECT
 constexpr int kMaxBand = 64;           // m*p <= 64
 constexpr int kVBufFloats = 8192;      // 32 KB vertical-pass buffer
 
@@ -111,7 +111,8 @@ resize_generic_kernel(KParams kp, const vp_clip_plan* __restrict__ plans, int n,
    if (kk < n) {
      const vp_clip_plan& q = plans[kk];
      const bool fast_ok = fast_aligned && q.kernel_variant != KV_GENERIC && ((clip_off[kk] | pitch_arr[kk]) & 15) == 0;
-     if (q.status == VP_OK && !fast_ok) my_tiles = clip_tiles(q.grid_t, q.grid_h, q.grid_w, kp.m);
+     if (q.status == VP_OK && !fast_ok && q.kernel_variant != KV_DIRECT)
+       my_tiles = clip_tiles(q.grid_t, q.grid_h, q.grid_w, kp.m);
    }
    // block exclusive scan of (my_tiles, owned)
    const int lane = tid & 31, wid = tid >> 5;
@@ -237,6 +238,90 @@ size_t generic_smem_bytes(int B) {
   return sizeof(float) * (kVBufFloats + 2 * (size_t)B * kMaxTaps) + sizeof(int) * (4 * B + 4);
 }
 
+// ------------------------------------------------------------------------------------------
+// KV_DIRECT: downscales whose windows exceed the generic kernel's weight tables (> ~34x on an axis; rare:
+// thumbnails of very large frames).  One thread per output pixel (all 3 channels) evaluates the separable
+// AA-bicubic sum straight from the u8 source in f64 (O4-O6, C10-C13: the same window, Keys weights and
+// renormalisation, no intermediate rounding), normalises, rounds once to the output dtype (O9) and stores into
+// every temporal slot the frame fills (O7).  Work ~ (4s)^2 per output pixel, i.e. ~16x the source pixels.
+// ------------------------------------------------------------------------------------------
+struct Axis {
+  int x0, x1;
+  double c, inv, rsum;                 // window, centre, 1/fs, 1 / sum of its Keys weights
+};
+__device__ __forceinline__ Axis direct_axis(int in, int out, int i) {
+  const double scale = (double)in / (double)out;
+  const double fs = scale > 1.0 ? scale : 1.0;
+  const double support = 2.0 * fs;
+  Axis a;
+  a.inv = 1.0 / fs;
+  a.c = ((double)i + 0.5) * scale;
+  a.x0 = max((int)(a.c - support + 0.5), 0);
+  a.x1 = min((int)(a.c + support + 0.5), in);
+  double s = 0.0;
+  for (int x = a.x0; x < a.x1; ++x) s += keys(((double)x - a.c + 0.5) * a.inv);
+  a.rsum = s != 0.0 ? 1.0 / s : 1.0;
+  return a;
+}
+
+template <bool kF32>
+__global__ void __launch_bounds__(256)
+resize_direct_kernel(KParams kp, const vp_clip_plan* __restrict__ plans, int n, const uint8_t* __restrict__ frames,
+                     const int64_t* __restrict__ clip_off, const int64_t* __restrict__ pitch_arr, void* pv_img,
+                     int64_t img_cap, void* pv_vid, int64_t vid_cap, double mean0, double mean1, double mean2,
+                     double std0, double std1, double std2) {
+  const int p = kp.p, m = kp.m, tp = kp.tp, D = kp.D;
+  const double mean[3] = {mean0, mean1, mean2}, sd[3] = {std0, std1, std2};
+  for (int k = blockIdx.y; k < n; k += gridDim.y) {
+    const vp_clip_plan pl = plans[k];
+    if (pl.status != VP_OK || pl.kernel_variant != KV_DIRECT) continue;
+    void* pv = pl.is_image ? pv_img : pv_vid;
+    const int64_t cap = pl.is_image ? img_cap : vid_cap;
+    if (pv == nullptr || pl.patch_offset + (int64_t)pl.grid_t * pl.grid_h * pl.grid_w > cap) continue;
+    const int64_t pitch = pitch_arr[k];
+    const int64_t hw = (int64_t)pl.out_h * pl.out_w;
+    const int64_t npx = (int64_t)pl.n_frames * hw;
+    const int gh = pl.grid_h / m, gw = pl.grid_w / m, B = m * p;
+    for (int64_t e = (int64_t)blockIdx.x * blockDim.x + threadIdx.x; e < npx; e += (int64_t)gridDim.x * blockDim.x) {
+      const int f = (int)(e / hw);
+      const int i = (int)((e - (int64_t)f * hw) / pl.out_w);
+      const int j = (int)(e - (int64_t)f * hw - (int64_t)i * pl.out_w);
+      const Axis av = direct_axis(pl.in_h, pl.out_h, i), ah = direct_axis(pl.in_w, pl.out_w, j);
+      const uint8_t* src = frames + clip_off[k] + (int64_t)f * pl.in_h * pitch;
+      double acc[3] = {0.0, 0.0, 0.0};
+      for (int y = av.x0; y < av.x1; ++y) {
+        const double wy = keys(((double)y - av.c + 0.5) * av.inv);
+        if (wy == 0.0) continue;
+        const uint8_t* row = src + (int64_t)y * pitch;
+        double r[3] = {0.0, 0.0, 0.0};
+        for (int x = ah.x0; x < ah.x1; ++x) {
+          const double wx = keys(((double)x - ah.c + 0.5) * ah.inv);
+          r[0] += wx * row[3 * x];
+          r[1] += wx * row[3 * x + 1];
+          r[2] += wx * row[3 * x + 2];
+        }
+#pragma unroll
+        for (int c = 0; c < 3; ++c) acc[c] += wy * r[c];
+      }
+      const int last = (f == pl.n_frames - 1) ? pl.grid_t * tp - 1 : f;   // frame n-1 fills the pad slots (O7)
+      const int hb = i / B, mh = (i / p) % m, py = i % p, wb = j / B, mw = (j / p) % m, px = j % p;
+#pragma unroll
+      for (int c = 0; c < 3; ++c) {
+        double v = acc[c] * av.rsum * ah.rsum;
+        v = v < 0.0 ? 0.0 : (v > 255.0 ? 255.0 : v);                        // C12
+        const float x = (float)((v / 255.0 - mean[c]) / sd[c]);              // O6 in f64, one rounding (O9)
+        for (int sl = f; sl <= last; ++sl) {
+          const int g = sl / tp, ti = sl - g * tp;
+          const int64_t r = pl.patch_offset + (((int64_t)g * gh + hb) * gw + wb) * m * m + mh * m + mw;
+          const int64_t q = ((int64_t)(c * tp + ti) * p + py) * p + px;
+          if (kF32) reinterpret_cast<float*>(pv)[r * D + q] = x;
+          else reinterpret_cast<__nv_bfloat16*>(pv)[r * D + q] = __double2bfloat16((v / 255.0 - mean[c]) / sd[c]);
+        }
+      }
+    }
+  }
+}
+
 // Grid outputs (H7) + per-clip status.  One small kernel; clips strided over threads.
 __global__ void grids_kernel(const vp_clip_plan* __restrict__ plans, int n, int64_t img_cap, int64_t vid_cap,
                              int has_img, int has_vid, int64_t* __restrict__ img_grid, int64_t* __restrict__ vid_grid,
@@ -248,9 +333,6 @@ __global__ void grids_kernel(const vp_clip_plan* __restrict__ plans, int n, int6
       const int64_t rows = (int64_t)pl.grid_t * pl.grid_h * pl.grid_w;
       const bool img = pl.is_image;
       if (!(img ? has_img : has_vid) || pl.patch_offset + rows > (img ? img_cap : vid_cap)) st = VP_ECAPACITY;
-      // generic clips: window length <= 4*max(in/out,1) + 2 taps must fit the weight tables (kMaxTaps)
-      const double fsv = fmax((double)pl.in_h / pl.out_h, 1.0), fsh = fmax((double)pl.in_w / pl.out_w, 1.0);
-      if (pl.kernel_variant == KV_GENERIC && 4.0 * fmax(fsv, fsh) + 2.0 > (double)kMaxTaps) st = VP_EUNSUPPORTED;
       int64_t* gptr = img ? img_grid : vid_grid;
       if (gptr != nullptr) {
         gptr[3 * pl.grid_index + 0] = pl.grid_t;
@@ -327,20 +409,38 @@ extern "C" vp_status vp_resize_normalize_patchify(const vp_params* p, const vp_c
   vp::grids_kernel<<<(n + 255) / 256, 256, 0, s>>>(plans, n, img_rows_cap, vid_rows_cap,
                                                    pixel_values_images != nullptr, pixel_values_videos != nullptr,
                                                    image_grid_thw, video_grid_thw, clip_status);
+  // launch hint (totals[VP_TOT_VARIANTS] of the plan): kernels of absent variants are not launched
+  const unsigned mask = p->launch_mask != 0 ? (unsigned)p->launch_mask : ~0u;
+  auto has = [&](int kv) { return (mask >> kv) & 1u; };
   const int fast_aligned = (reinterpret_cast<uintptr_t>(frames) & 15) == 0;
-  if (fast_aligned) {
+  const bool any_fast = has(vp::KV_MILD) || has(vp::KV_MEDIUM) || has(vp::KV_STRONG) || has(vp::KV_COPY) ||
+                        has(vp::KV_TEAM) || has(vp::KV_WIDE);
+  if (fast_aligned && any_fast) {
     const vp::FKParams fk = vp::make_fkparams(p);
     cudaError_t e = vp::launch_index(plans, n, clip_byte_offset, row_pitch, ws, s);
-    if (e == cudaSuccess)
+    if (e == cudaSuccess && (has(vp::KV_TEAM) || has(vp::KV_WIDE)))
       e = vp::launch_team(fk, plans, n, ws, frames, clip_byte_offset, row_pitch, pixel_values_images, img_rows_cap,
-                          pixel_values_videos, vid_rows_cap, clip_status, dev, sms, s);
+                          pixel_values_videos, vid_rows_cap, clip_status, dev, sms, mask, s);
     if (e == cudaSuccess)
       e = vp::launch_fast_variants(fk, plans, n, ws, frames, clip_byte_offset, row_pitch, pixel_values_images,
-                                   img_rows_cap, pixel_values_videos, vid_rows_cap, dev, sms, s);
+                                   img_rows_cap, pixel_values_videos, vid_rows_cap, dev, sms, mask, s);
     if (e != cudaSuccess) {
       vp::set_error("vp_resize_normalize_patchify: %s", cudaGetErrorString(e));
       return VP_ECUDA;
     }
+  }
+  if (has(vp::KV_DIRECT)) {
+    const dim3 dg(16, (unsigned)(n < 65535 ? n : 65535));
+    if (kp.out_f32)
+      vp::resize_direct_kernel<true><<<dg, 256, 0, s>>>(kp, plans, n, frames, clip_byte_offset, row_pitch,
+                                                        pixel_values_images, img_rows_cap, pixel_values_videos,
+                                                        vid_rows_cap, p->mean[0], p->mean[1], p->mean[2], p->std[0],
+                                                        p->std[1], p->std[2]);
+    else
+      vp::resize_direct_kernel<false><<<dg, 256, 0, s>>>(kp, plans, n, frames, clip_byte_offset, row_pitch,
+                                                         pixel_values_images, img_rows_cap, pixel_values_videos,
+                                                         vid_rows_cap, p->mean[0], p->mean[1], p->mean[2], p->std[0],
+                                                         p->std[1], p->std[2]);
   }
   const int grid = sms * 3;
   const size_t smem = vp::generic_smem_bytes(kp.m * kp.p);

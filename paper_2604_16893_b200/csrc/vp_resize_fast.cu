@@ -44,6 +44,9 @@
 #ifndef VP_HREGS
 #define VP_HREGS 104
 #endif
+#ifndef VP_ALL_LANES_ARRIVE
+#define VP_ALL_LANES_ARRIVE 0   // verification build only (scripts/sanitize.sh): every lane arrives on vfull/vempty
+#endif
 #ifndef VP_EXP_NO_VMATH
 #define VP_EXP_NO_VMATH 0   // experiments only: skip the V ring FMAs
 #endif
@@ -229,7 +232,8 @@ struct FastCfg {
   static constexpr size_t OFF_HX = OFF_WH + (size_t)kWhFloats * 4;
   static constexpr size_t OFF_BAR = (OFF_HX + (size_t)MAXWS * 4 + 15) & ~(size_t)15;
   static constexpr size_t OFF_PROD = OFF_BAR + (kNVW * kNGrp + 2 * (kCapR / 2)) * 8;   // ProdState [kNVW]
-  static constexpr size_t SMEM = OFF_PROD + (size_t)kNVW * 32;
+  static constexpr size_t OFF_EBAR = OFF_PROD + (size_t)kNVW * 32;                      // verification build only
+  static constexpr size_t SMEM = OFF_EBAR + (size_t)kNVW * kNGrp * 8;
   static_assert(OFF_VBUF % 16 == 0 && OFF_WROW % 16 == 0 && OFF_WH % 16 == 0, "align");
   static_assert(SMEM + 1024 <= 228 * 1024 / 2, "two CTAs per SM");
 };
@@ -307,6 +311,7 @@ resize_fast_kernel(FKParams kp, const vp_clip_plan* __restrict__ plans, const VI
   int* hx = reinterpret_cast<int*>(smem + Cfg::OFF_HX);
   uint64_t* full_all = reinterpret_cast<uint64_t*>(smem + Cfg::OFF_BAR);   // [kNVW][kDepth]
   uint64_t* vfull = full_all + kNVW * kNGrp;                                // retired row pairs: V -> H
+  uint64_t* ebar_all = reinterpret_cast<uint64_t*>(smem + Cfg::OFF_EBAR);  // [kNVW][kNGrp] (VP_ALL_LANES_ARRIVE)
   uint64_t* vempty = vfull + kCapR / 2;                                     // H -> V
 
   const int tid = threadIdx.x;
@@ -323,10 +328,13 @@ resize_fast_kernel(FKParams kp, const vp_clip_plan* __restrict__ plans, const VI
   const int64_t my_b = total * (blockIdx.x + 1) / gridDim.x;
 
   if (tid == 0) {
-    for (int s = 0; s < kNVW * kNGrp; ++s) mbar_init(&full_all[s], 1);
+    for (int s = 0; s < kNVW * kNGrp; ++s) {
+      mbar_init(&full_all[s], 1);
+      mbar_init(&ebar_all[s], 32);
+    }
     for (int s = 0; s < kCapR / 2; ++s) {
-      mbar_init(&vfull[s], 2 * kNVW);      // each V warp arrives once per row of the pair
-      mbar_init(&vempty[s], kNHW);
+      mbar_init(&vfull[s], 2 * kNVW * (VP_ALL_LANES_ARRIVE ? 32 : 1));   // each V warp arrives once per row of the pair
+      mbar_init(&vempty[s], kNHW * (VP_ALL_LANES_ARRIVE ? 32 : 1));
     }
     asm volatile("fence.mbarrier_init.release.cluster;" ::: "memory");
   }
@@ -338,6 +346,7 @@ resize_fast_kernel(FKParams kp, const vp_clip_plan* __restrict__ plans, const VI
     asm volatile("setmaxnreg.inc.sync.aligned.u32 %0;\n" :: "n"(VP_VREGS) : "memory");
     uint8_t* stage = stage_all + (size_t)warp * kDepth * kWarpB;
     uint64_t* full = full_all + warp * kNGrp;     // one barrier per group of kGrp staging slots
+    uint64_t* ebar = ebar_all + warp * kNGrp;     // verification build: the warp's reads of a group are done
     uint32_t rc = 0;                  // staged rows read so far: slot rc % kDepth, phase (rc / kDepth) & 1
     uint32_t vslot = 0, vphase = 0;   // vbuf slot of the next retired row and its pair phase (kCapR even:
                                       // vslot & 1 is the row's parity within its pair)
@@ -348,6 +357,14 @@ resize_fast_kernel(FKParams kp, const vp_clip_plan* __restrict__ plans, const VI
     ProdState* ps = reinterpret_cast<ProdState*>(smem + Cfg::OFF_PROD) + warp;
     if (l0) *ps = ProdState{nullptr, 0, my_a, 0, 0};
     __syncwarp();
+    // verification build (compute-sanitizer racecheck): every lane arrives on ebar[g] after reading group g and
+    // waits for the phase before the TMA refill (the shipped kernel relies on the __syncwarp before the refill)
+    auto reads_done = [&](uint32_t g, uint32_t parity) {
+      if (VP_ALL_LANES_ARRIVE) {
+        mbar_arrive(&ebar[g]);
+        mbar_wait(&ebar[g], parity);
+      }
+    };
     auto issue_group = [&](uint32_t g) {          // refill the kGrp slots of group g, then arrive once
       // opaque copy of g (nvcc 12.9 CSE workaround, see vp_resize_ring.cu)
       asm volatile("mov.b32 %0, %0;" : "+r"(g));
@@ -472,6 +489,7 @@ resize_fast_kernel(FKParams kp, const vp_clip_plan* __restrict__ plans, const VI
               const uint32_t used = rc++ % kDepth;                                              \
               if ((used & (kGrp - 1)) == kGrp - 1) {   /* group read: refill it */                \
                 __syncwarp();                                                                   \
+                reads_done(used / kGrp, ((rc - 1) / kDepth) & 1);                               \
                 issue_group(used / kGrp);                                                       \
               }                                                                                 \
               const float w5[kRing] = {wa.x, wa.y, wa.z, wa.w, wb};                             \
@@ -482,7 +500,7 @@ resize_fast_kernel(FKParams kp, const vp_clip_plan* __restrict__ plans, const VI
             if (VP_PLANAR) retire_planar<U>(acc, reinterpret_cast<float*>(vbuf + vs * kRowPx), px_lane, vactive); \
             else retire_slot<U>(acc, vbuf + vs * kRowPx, vb, vactive);                          \
             __syncwarp();                                                                       \
-            if (lane == 0) mbar_arrive(&vfull[vp2]);                                            \
+            if (lane == 0 || VP_ALL_LANES_ARRIVE) mbar_arrive(&vfull[vp2]);                                            \
             if (++vslot == kCapR) { vslot = 0; vphase ^= 1; }                                   \
           }
           static_assert(kRing == 5, "unroll below");
@@ -491,7 +509,7 @@ resize_fast_kernel(FKParams kp, const vp_clip_plan* __restrict__ plans, const VI
         }
         if (vslot & 1) {                            // odd out_h: complete the last pair's barrier phase
           __syncwarp();
-          if (lane == 0) mbar_arrive(&vfull[vslot >> 1]);
+          if (lane == 0 || VP_ALL_LANES_ARRIVE) mbar_arrive(&vfull[vslot >> 1]);
           if (++vslot == kCapR) { vslot = 0; vphase ^= 1; }
         }
         // source rows below the last window (none for the supported ratios) keep the ring in step
@@ -501,6 +519,7 @@ resize_fast_kernel(FKParams kp, const vp_clip_plan* __restrict__ plans, const VI
           const uint32_t used = rc++ % kDepth;
           if ((used & (kGrp - 1)) == kGrp - 1) {
             __syncwarp();
+            reads_done(used / kGrp, ((rc - 1) / kDepth) & 1);
             issue_group(used / kGrp);
           }
         }
@@ -690,7 +709,7 @@ resize_fast_kernel(FKParams kp, const vp_clip_plan* __restrict__ plans, const VI
           }
         }
         __syncwarp();
-        if (lane == 0) mbar_arrive(&vempty[s0 >> 1]);
+        if (lane == 0 || VP_ALL_LANES_ARRIVE) mbar_arrive(&vempty[s0 >> 1]);
         vrow += 2;                                  // V pads an odd last row, so pairs stay aligned
       }
     }
@@ -874,18 +893,20 @@ FKParams make_fkparams(const vp_params* p) {
 // that variant's items only (work index built by launch_index in the same workspace).
 cudaError_t launch_fast_variants(const FKParams& kp, const vp_clip_plan* plans, int n, const ResizeWs& w,
                                  const uint8_t* frames, const int64_t* coff, const int64_t* pitch, void* pi,
-                                 int64_t icap, void* pvv, int64_t vcap, int dev, int num_sms, cudaStream_t s) {
+                                 int64_t icap, void* pvv, int64_t vcap, int dev, int num_sms, unsigned mask,
+                                 cudaStream_t s) {
   auto vx = [&](int slot) { return ws_vidx(w, n, slot); };
+  auto has = [&](int kv) { return ((mask >> kv) & 1u) != 0; };
   if (kp.out_f32) {
-    launch_fast<KV_MILD, true>(kp, plans, vx(0), frames, coff, pitch, pi, icap, pvv, vcap, dev, num_sms, s);
-    launch_fast<KV_MEDIUM, true>(kp, plans, vx(1), frames, coff, pitch, pi, icap, pvv, vcap, dev, num_sms, s);
-    launch_fast<KV_STRONG, true>(kp, plans, vx(2), frames, coff, pitch, pi, icap, pvv, vcap, dev, num_sms, s);
-    launch_copy<true>(kp, plans, vx(3), frames, coff, pitch, pi, icap, pvv, vcap, dev, num_sms, s);
+    if (has(KV_MILD)) launch_fast<KV_MILD, true>(kp, plans, vx(0), frames, coff, pitch, pi, icap, pvv, vcap, dev, num_sms, s);
+    if (has(KV_MEDIUM)) launch_fast<KV_MEDIUM, true>(kp, plans, vx(1), frames, coff, pitch, pi, icap, pvv, vcap, dev, num_sms, s);
+    if (has(KV_STRONG)) launch_fast<KV_STRONG, true>(kp, plans, vx(2), frames, coff, pitch, pi, icap, pvv, vcap, dev, num_sms, s);
+    if (has(KV_COPY)) launch_copy<true>(kp, plans, vx(3), frames, coff, pitch, pi, icap, pvv, vcap, dev, num_sms, s);
   } else {
-    launch_fast<KV_MILD, false>(kp, plans, vx(0), frames, coff, pitch, pi, icap, pvv, vcap, dev, num_sms, s);
-    launch_fast<KV_MEDIUM, false>(kp, plans, vx(1), frames, coff, pitch, pi, icap, pvv, vcap, dev, num_sms, s);
-    launch_fast<KV_STRONG, false>(kp, plans, vx(2), frames, coff, pitch, pi, icap, pvv, vcap, dev, num_sms, s);
-    launch_copy<false>(kp, plans, vx(3), frames, coff, pitch, pi, icap, pvv, vcap, dev, num_sms, s);
+    if (has(KV_MILD)) launch_fast<KV_MILD, false>(kp, plans, vx(0), frames, coff, pitch, pi, icap, pvv, vcap, dev, num_sms, s);
+    if (has(KV_MEDIUM)) launch_fast<KV_MEDIUM, false>(kp, plans, vx(1), frames, coff, pitch, pi, icap, pvv, vcap, dev, num_sms, s);
+    if (has(KV_STRONG)) launch_fast<KV_STRONG, false>(kp, plans, vx(2), frames, coff, pitch, pi, icap, pvv, vcap, dev, num_sms, s);
+    if (has(KV_COPY)) launch_copy<false>(kp, plans, vx(3), frames, coff, pitch, pi, icap, pvv, vcap, dev, num_sms, s);
   }
   return cudaGetLastError();
 }

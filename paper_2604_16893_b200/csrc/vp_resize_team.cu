@@ -45,6 +45,12 @@ constexpr int kNR = VP_TEAM_NR;             // retire slots (rows V may run ahea
 #ifndef VP_TEAM_HINT
 #define VP_TEAM_HINT 0      // suspend-time hint (ns) of the V<->H retire-slot waits; 0 = spin
 #endif
+// Verification build only (scripts/sanitize.sh): every lane arrives on the retire-slot barriers instead of lane 0
+// after __syncwarp (equivalent under the PTX memory model -- bar.warp.sync orders the warp's shared-memory writes
+// before lane 0's release -- but compute-sanitizer racecheck only credits a thread's own arrive).
+#ifndef VP_ALL_LANES_ARRIVE
+#define VP_ALL_LANES_ARRIVE 0
+#endif
 
 template <int NV, int NH>
 struct SplitCfg {
@@ -58,7 +64,8 @@ struct SplitCfg {
   static constexpr size_t OFF_RBAR = OFF_SBAR + (size_t)kTNGrp * 8;
   static constexpr size_t OFF_CNT = OFF_RBAR + (size_t)2 * kNR * 8;
   static constexpr size_t OFF_PROD = (OFF_CNT + (size_t)kTNGrp * 4 + 15) & ~(size_t)15;
-  static constexpr size_t SMEM = OFF_PROD + 48;
+  static constexpr size_t OFF_EBAR = OFF_PROD + 48;   // staging "read" barriers (VP_ALL_LANES_ARRIVE build only)
+  static constexpr size_t SMEM = OFF_EBAR + (size_t)kTNGrp * 8;
   static_assert(OFF_WREC % 16 == 0 && OFF_BUF % 16 == 0 && OFF_SBAR % 8 == 0 && OFF_PROD % 16 == 0, "align");
 };
 
@@ -210,6 +217,7 @@ resize_split_kernel(FKParams kp, const vp_clip_plan* __restrict__ plans, const V
   uint64_t* rfull = reinterpret_cast<uint64_t*>(smem + Cfg::OFF_RBAR);      // V -> H: retire slot filled
   uint64_t* rempty = rfull + kNR;                                           // H -> V: retire slot released
   int* gcnt = reinterpret_cast<int*>(smem + Cfg::OFF_CNT);                  // V warps done with a staging group
+  uint64_t* sread = reinterpret_cast<uint64_t*>(smem + Cfg::OFF_EBAR);      // verification build: group read
   TeamProd* ps = reinterpret_cast<TeamProd*>(smem + Cfg::OFF_PROD);
   float4* buf0 = reinterpret_cast<float4*>(smem + Cfg::OFF_BUF);
   const uint32_t buf_s = smem_u32(buf0);
@@ -264,10 +272,10 @@ resize_split_kernel(FKParams kp, const vp_clip_plan* __restrict__ plans, const V
   };
 
   if (tid == 0) {
-    for (int i = 0; i < kTNGrp; ++i) { mbar_init(&sfull[i], 1); gcnt[i] = 0; }
+    for (int i = 0; i < kTNGrp; ++i) { mbar_init(&sfull[i], 1); mbar_init(&sread[i], NV * 32); gcnt[i] = 0; }
     for (int i = 0; i < kNR; ++i) {
-      mbar_init(&rfull[i], NV);
-      mbar_init(&rempty[i], NH);
+      mbar_init(&rfull[i], VP_ALL_LANES_ARRIVE ? NV * 32 : NV);
+      mbar_init(&rempty[i], VP_ALL_LANES_ARRIVE ? NH * 32 : NH);
     }
     asm volatile("fence.mbarrier_init.release.cluster;" ::: "memory");
     TeamProd z;
@@ -301,7 +309,8 @@ resize_split_kernel(FKParams kp, const vp_clip_plan* __restrict__ plans, const V
         for (int q = 0; q < 3; ++q) acc[r][q] = make_float4(0.f, 0.f, 0.f, 0.f);
       int y = 0;
       // after the last row of group g: the last V warp to finish it refills it
-      auto group_done = [&](uint32_t g) {
+      auto group_done = [&](uint32_t g, uint32_t parity) {
+        if (VP_ALL_LANES_ARRIVE) mbar_arrive(&sread[g]);   // verification build: this lane's reads of g are done
         __syncwarp();
         int old = 0;
         if (l0) {
@@ -309,7 +318,10 @@ resize_split_kernel(FKParams kp, const vp_clip_plan* __restrict__ plans, const V
           old = atomicAdd(&gcnt[g], 1);
           if (old == NV - 1) gcnt[g] = 0;
         }
-        if (__shfl_sync(0xffffffffu, old, 0) == NV - 1) issue_group(g);
+        if (__shfl_sync(0xffffffffu, old, 0) == NV - 1) {
+          if (VP_ALL_LANES_ARRIVE) mbar_wait_uni(&sread[g], parity);
+          issue_group(g);
+        }
       };
 #define VP_V_BODY(U)                                                                                         \
       {                                                                                                       \
@@ -321,7 +333,7 @@ resize_split_kernel(FKParams kp, const vp_clip_plan* __restrict__ plans, const V
         float2 fv[6];                                                                                         \
         cvt_ring(n0, n1, n2, fv);                                                                             \
         ++rc;                                                                                                 \
-        if ((slot & (kTGrp - 1)) == kTGrp - 1) group_done(slot / kTGrp);                                      \
+        if ((slot & (kTGrp - 1)) == kTGrp - 1) group_done(slot / kTGrp, ((rc - 1) / kTDepth) & 1);             \
         ring4<U>(acc, wv, fv);                                                                                \
       }
 #define VP_V_RETIRE(U)                                                                                       \
@@ -336,7 +348,7 @@ resize_split_kernel(FKParams kp, const vp_clip_plan* __restrict__ plans, const V
         sts_f4(ra + 384, make_float4(a[0].w, a[1].w, a[2].w, 0.f));                                           \
         _Pragma("unroll") for (int q = 0; q < 3; ++q) acc[U][q] = make_float4(0.f, 0.f, 0.f, 0.f);            \
         __syncwarp();                                                                                         \
-        mbar_arrive_if(&rfull[rs], l0);                                                                       \
+        mbar_arrive_if(&rfull[rs], l0 || VP_ALL_LANES_ARRIVE);                                                \
         ++rr;                                                                                                 \
       }
       int4 ye_next = __ldg(reinterpret_cast<const int4*>(y1));
@@ -361,7 +373,7 @@ resize_split_kernel(FKParams kp, const vp_clip_plan* __restrict__ plans, const V
         if ((rc & (kTGrp - 1)) == 0) mbar_wait_uni(&sfull[(rc / kTGrp) % kTNGrp], (rc / kTDepth) & 1);
         const uint32_t slot = rc % kTDepth;
         ++rc;
-        if ((slot & (kTGrp - 1)) == kTGrp - 1) group_done(slot / kTGrp);
+        if ((slot & (kTGrp - 1)) == kTGrp - 1) group_done(slot / kTGrp, ((rc - 1) / kTDepth) & 1);
       }
 #undef VP_V_BODY
 #undef VP_V_RETIRE
@@ -472,7 +484,7 @@ resize_split_kernel(FKParams kp, const vp_clip_plan* __restrict__ plans, const V
           mbar_wait_uni<VP_TEAM_HINT>(&rfull[sbase + U], par);
           hrow((sbase + (uint32_t)U) * kSlotB, qb);
           __syncwarp();
-          mbar_arrive_if(&rempty[sbase + U], l0);
+          mbar_arrive_if(&rempty[sbase + U], l0 || VP_ALL_LANES_ARRIVE);
         }
         rr += 4;
       }
@@ -486,7 +498,7 @@ resize_split_kernel(FKParams kp, const vp_clip_plan* __restrict__ plans, const V
           qb[pp] = fbase + (int64_t)((i / B) * hb_stride + ((i / p) % m) * m * D + (i % p) * p + colpart[pp]) * kEsz;
         hrow(rs * kSlotB, qb);
         __syncwarp();
-        mbar_arrive_if(&rempty[rs], l0);
+        mbar_arrive_if(&rempty[rs], l0 || VP_ALL_LANES_ARRIVE);
         ++rr;
       }
     }
@@ -736,20 +748,25 @@ void launch_split(const FKParams& kp, bool preset, const vp_clip_plan* plans, co
 
 cudaError_t launch_team(const FKParams& kp, const vp_clip_plan* plans, int n, const ResizeWs& w, const uint8_t* frames,
                         const int64_t* coff, const int64_t* pitch, void* pi, int64_t icap, void* pvv, int64_t vcap,
-                        int32_t* clip_status, int dev, int num_sms, cudaStream_t s) {
+                        int32_t* clip_status, int dev, int num_sms, unsigned mask, cudaStream_t s) {
   dim3 tg((kTabInH + 127) / 128, n);
   team_vtab_kernel<<<tg, 128, 0, s>>>(plans, coff, pitch, w.alias, w.vtab, w.y1tab, w.tflag);
   const bool preset = kp.p == 16 && kp.m == 2 && kp.tp == 2;
+  const bool team = (mask >> KV_TEAM) & 1u, wide = (mask >> KV_WIDE) & 1u;
   if (kp.out_f32) {
-    launch_split<kTeamNV, kTeamNH, kTeamPPL, 2, true>(kp, preset, plans, ws_vidx(w, n, 4), w, frames, coff, pitch, pi, icap,
-                                            pvv, vcap, clip_status, dev, num_sms, s);
-    launch_split<kWideNV, kWideNH, kWidePPL, 1, true>(kp, preset, plans, ws_vidx(w, n, 5), w, frames, coff, pitch, pi, icap,
-                                            pvv, vcap, clip_status, dev, num_sms, s);
+    if (team)
+      launch_split<kTeamNV, kTeamNH, kTeamPPL, 2, true>(kp, preset, plans, ws_vidx(w, n, 4), w, frames, coff, pitch, pi,
+                                                        icap, pvv, vcap, clip_status, dev, num_sms, s);
+    if (wide)
+      launch_split<kWideNV, kWideNH, kWidePPL, 1, true>(kp, preset, plans, ws_vidx(w, n, 5), w, frames, coff, pitch, pi,
+                                                        icap, pvv, vcap, clip_status, dev, num_sms, s);
   } else {
-    launch_split<kTeamNV, kTeamNH, kTeamPPL, 2, false>(kp, preset, plans, ws_vidx(w, n, 4), w, frames, coff, pitch, pi, icap,
-                                             pvv, vcap, clip_status, dev, num_sms, s);
-    launch_split<kWideNV, kWideNH, kWidePPL, 1, false>(kp, preset, plans, ws_vidx(w, n, 5), w, frames, coff, pitch, pi, icap,
-                                             pvv, vcap, clip_status, dev, num_sms, s);
+    if (team)
+      launch_split<kTeamNV, kTeamNH, kTeamPPL, 2, false>(kp, preset, plans, ws_vidx(w, n, 4), w, frames, coff, pitch, pi,
+                                                         icap, pvv, vcap, clip_status, dev, num_sms, s);
+    if (wide)
+      launch_split<kWideNV, kWideNH, kWidePPL, 1, false>(kp, preset, plans, ws_vidx(w, n, 5), w, frames, coff, pitch, pi,
+                                                         icap, pvv, vcap, clip_status, dev, num_sms, s);
   }
   return cudaGetLastError();
 }
