@@ -191,7 +191,7 @@ def run_ours(args, rank, world, local_rank):
             work.wait()                                        # the compute stream waits for the gather here
             vp.pack_offsets(gathered, world, per, tok_off, pat_off)
 
-    launches_per_step = 5 + (2 if world > 1 else 0)
+    launches_per_step = k3_launches(int(pl.totals["variants"]), per) + 4 + (2 if world > 1 else 0)   # + K1 (2), K4 (2)
     for _ in range(args.warmup):
         step()
     torch.cuda.synchronize()
@@ -227,6 +227,12 @@ def run_ours(args, rank, world, local_rank):
         e2e = run_e2e(args, pre, pl, frames, off, pitch, out, tt, cu, pos, deltas, rst, ws, per, dev, world,
                       tokens_rank)
 
+    # ---------------- N3: the same job with GRPO dedup (64 prompts x 8 rollouts, P:73 / P:271) ----------------
+    dedup = None
+    if not args.no_dedup and args.config == "cfg5":
+        dedup = run_dedup(args, pre, pl, frames, off_d, pitch_d, tt, cu, pos, deltas, rst, ws, per, a, dev, world,
+                          tokens_rank)
+
     result = None
     if rank == 0:
         peak, peak_src = peaks()
@@ -252,8 +258,83 @@ def run_ours(args, rank, world, local_rank):
             "gpu_launches": launches_per_step * args.steps,
             "clocks": clk,
             "e2e": e2e,
+            "dedup_64x8": dedup,
         }
     return result
+
+
+def k3_launches(mask: int, n: int) -> int:
+    """Kernels one vp_resize_normalize_patchify call launches for a plan whose kernel-variant mask is `mask`
+    (mirrors the dispatch in vp_resize.cu): grids + generic always; the work index when any TMA variant is present;
+    the team tables when team/wide clips are; one launch per present TMA variant; the direct kernel if needed."""
+    has = lambda v: (mask >> v) & 1
+    tma = [has(v) for v in (0, 1, 2, 4, 5, 6)]          # mild, medium, strong, copy, team, wide
+    n_l = 2 + (1 if any(tma) else 0) + sum(tma) + (1 if (has(5) or has(6)) else 0) + has(7)
+    return n_l if n > 0 else 0
+
+
+def run_dedup(args, pre, pl, frames, off_d, pitch_d, tt, cu, pos, deltas, rst, ws, per, a, dev, world, tokens_rank):
+    """cfg5 as GRPO delivers it: sample s of the job is rollout s % 8 of prompt s // 8, keyed by its prompt.  One step
+    = vp_dedup_clips over the rank's samples + K1 over the unique clips + K3 over the unique clips only (their frames
+    are the first rollout's, already resident) + vp_dedup_views (per-sample patch offset and grid) + K4 over every
+    sample's sequence.  The unique-clip list is a function of the keys; it is read back once before timing (a
+    trainer knows it from the prompt ids).  Value = tokens delivered to all samples / step time."""
+    import torch
+    import torch.distributed as dist
+    import paper_2604_16893_b200 as vp
+    rollouts = 8
+    keys = [(a + k) // rollouts for k in range(per)]
+    samples = [cfg5_clip()] * per
+    uclips, ulist, uid = pre.dedup(samples, keys)
+    upl = pre.plan(uclips)
+    P = pre.launch_params(upl)
+    uout = pre.alloc_outputs(upl)
+    ul = torch.tensor(ulist, dtype=torch.int64, device=dev)
+    uoff, upitch = off_d[ul], pitch_d[ul]
+    keys_d = torch.tensor(keys, dtype=torch.int64, device=dev)
+    uid_d = torch.empty(per, dtype=torch.int32, device=dev)
+    ulist_d = torch.empty(per, dtype=torch.int32, device=dev)
+    nu_d = torch.empty(1, dtype=torch.int32, device=dev)
+    po = torch.empty(per, dtype=torch.int64, device=dev)
+    grid = torch.empty(per, 3, dtype=torch.int64, device=dev)
+    stream = torch.cuda.current_stream(dev)
+    nu = len(ulist)
+
+    def step():
+        vp.dedup_clips(keys_d, uid_d, ulist_d, nu_d)
+        vp.plan_frames(P, upl.clips_dev, nu, upl.plans_dev, upl.frame_indices, upl.totals_dev, upl.group_timestamps)
+        vp.resize_normalize_patchify(P, upl.plans_dev, nu, frames, uoff, upitch, None, uout["pixel_values_videos"],
+                                     uout["image_grid_thw"], uout["video_grid_thw"], uout["clip_status"],
+                                     workspace=uout["workspace"])
+        vp.dedup_views(upl.plans_dev, uid_d, po, grid)
+        vp.rope_index(P, vp.VP_ROPE_QWEN3_SPLIT, tt, cu, None, grid, pos, deltas, rst, ws)
+
+    for _ in range(args.warmup):
+        step()
+    torch.cuda.synchronize()
+    assert (uout["clip_status"][:nu].cpu().numpy() == 0).all() and (rst.cpu().numpy() == 0).all()
+    if world > 1:
+        dist.barrier()
+    t0 = torch.cuda.Event(enable_timing=True)
+    t1 = torch.cuda.Event(enable_timing=True)
+    t0.record(stream)
+    for _ in range(args.steps):
+        step()
+    t1.record(stream)
+    torch.cuda.synchronize()
+    ms = t0.elapsed_time(t1) / args.steps
+    t = torch.tensor([ms], dtype=torch.float64, device=dev)
+    if world > 1:
+        dist.all_reduce(t, op=dist.ReduceOp.MAX)
+    ms = float(t.item())
+    ph = upl.plans_host
+    k3_bytes = int(sum(int(ph["n_frames"][k]) * int(ph["in_h"][k]) * 3 * int(ph["in_w"][k]) for k in range(nu))
+                   + upl.totals["vid_rows"] * pre.D * 2)
+    return {"value": tokens_rank * world / (ms * 1e-3), "unit": UNIT, "ms_per_step": ms, "steps": args.steps,
+            "samples_per_rank": per, "unique_clips_per_rank": nu, "rollouts_per_prompt": rollouts,
+            "k3_algorithmic_bytes_per_step": k3_bytes,
+            "note": "tokens counted per delivered sample; K3 reads/writes the unique clips only (P:73 hash-based "
+                    "dedup); not the headline (the default line processes every sample)"}
 
 
 def load_traffic(clips_per_rank):
@@ -425,6 +506,7 @@ def main():
     ap.add_argument("--e2e-steps", type=int, default=2)
     ap.add_argument("--e2e-chunk", type=int, default=8)
     ap.add_argument("--no-cpu-baseline", action="store_true")
+    ap.add_argument("--no-dedup", action="store_true", help="skip the 64 x 8 GRPO dedup line (N3)")
     ap.add_argument("--cpu-clips", type=int, default=4)
     ap.add_argument("--ref-groups", type=int, default=2)
     ap.add_argument("--backend", default="nccl", choices=["nccl", "gloo"],

@@ -234,6 +234,25 @@ vp_status vp_plan_records(const vp_clip_plan* plans, int32_t n, int32_t merge_si
                           int32_t* records, void* stream);
 
 /* ---------------------------------------------------------------------------------------------
+ * vp_dedup_clips -- N3: hash-based deduplication of a batch ("hash-based deduplication"; GRPO n = 8 rollouts
+ * per prompt).  keys (dev) [n] uint64: one caller-chosen key per sample's clip (e.g. a hash of the video id
+ * and the sampling parameters; the library does not hash frame bytes -- reading them costs as much as processing
+ * them).  Outputs: unique_id (dev) [n] int32 = dense id of the sample's key in order of first occurrence;
+ * unique_list (dev) [n] int32, first *n_unique entries = the batch index of each key's first occurrence, in batch
+ * order; n_unique (dev) int32.  The caller plans and resizes clips[unique_list[0..U)] only.  One CTA; O(n^2 / 1024)
+ * key compares per thread.  Errors: VP_EINVAL, VP_ECUDA.
+ *
+ * vp_dedup_views -- per sample, its view into the unique clips' outputs: patch_offset (dev) [n] int64 (first row
+ * in the unique pixel_values of its modality; -1 if the clip is invalid), grid_thw (dev) [n,3] int64 (the sample's
+ * grid, e.g. for vp_rope_index over every sample's sequence), status (dev, nullable) [n] int32 (plan status).
+ * unique_plans (dev) [U] from vp_plan_frames over the unique clips; unique_id from vp_dedup_clips.
+ * ------------------------------------------------------------------------------------------- */
+vp_status vp_dedup_clips(const uint64_t* keys, int32_t n, int32_t* unique_id, int32_t* unique_list,
+                         int32_t* n_unique, void* stream);
+vp_status vp_dedup_views(const vp_clip_plan* unique_plans, const int32_t* unique_id, int32_t n,
+                         int64_t* patch_offset, int64_t* grid_thw, int32_t* status, void* stream);
+
+/* ---------------------------------------------------------------------------------------------
  * vp_synth_frames -- test/bench input generator (not part of the hot path; never timed).
  *   RAMP: (seed*2654435761 + i*97 + y*31 + x*7 + c) mod 256, i = frame_ids[f]
  *   NOISE : top 8 bits of splitmix64(((i*H + y)*W + x)*3 + c + seed*0xD1B54A32D192ED03)

@@ -31,6 +31,7 @@ __all__ = [
     "keys_cubic", "aa_weights", "weight_matrix", "resize_frame", "resize_pixel",
     "normalize", "temporal_pad", "patchify", "patch_coords", "bf16_rne_bits", "bf16_bits_to_f64",
     "group_timestamps", "second_per_grid", "qwen25_interval", "rope_index", "process_batch", "ClipPlan",
+    "dedup_keys",
 ]
 
 VP_OK, VP_EINVAL, VP_EMISMATCH = 0, 1, 3
@@ -479,3 +480,20 @@ def process_batch(params: dict, clips, frames_list, plans=None):
                 image_grid_thw=np.array(img_grids, dtype=np.int64).reshape(-1, 3),
                 video_grid_thw=np.array(vid_grids, dtype=np.int64).reshape(-1, 3),
                 plans=plans, totals=totals)
+
+
+# ---------------------------------------------------------------------------
+# N3 -- hash-based deduplication of a batch ("hash-based deduplication"; GRPO n rollouts per prompt)
+# ---------------------------------------------------------------------------
+
+def dedup_keys(keys):
+    """Keep the first occurrence of each key.  Returns (unique_id per sample = rank of its key's first occurrence
+    among first occurrences, unique_list = batch indices of the first occurrences in batch order)."""
+    first = {}
+    unique_list, unique_id = [], []
+    for k, key in enumerate(keys):
+        if key not in first:
+            first[key] = len(unique_list)
+            unique_list.append(k)
+        unique_id.append(first[key])
+    return unique_id, unique_list

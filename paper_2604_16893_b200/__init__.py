@@ -21,7 +21,8 @@ from ._lib import (DESC_DTYPE, PLAN_DTYPE, TOT, TOT_LEN, VP_BUDGET_PER_FRAME, VP
 __all__ = [
     "make_params", "clip_desc_array", "plan_frames", "resize_normalize_patchify", "resize_workspace_bytes",
     "resize_workspace", "rope_index",
-    "rope_index_workspace_bytes", "plan_records", "pack_offsets", "synth_frames", "VisualPreprocessor",
+    "rope_index_workspace_bytes", "plan_records", "pack_offsets", "synth_frames", "dedup_clips", "dedup_views",
+    "VisualPreprocessor",
     "PlacementMismatch", "VpError", "VpParams", "DESC_DTYPE", "PLAN_DTYPE", "TOT", "TOT_LEN",
     "VP_ROPE_QWEN3_SPLIT", "VP_ROPE_QWEN2", "VP_ROPE_QWEN25", "VP_OUT_BF16", "VP_OUT_F32",
     "VP_BUDGET_PER_FRAME", "VP_BUDGET_TOTAL", "VP_SYNTH_RAMP", "VP_SYNTH_NOISE", "VP_OK", "VP_EINVAL",
@@ -146,6 +147,18 @@ def synth_frames(kind: int, seed: int, frame_ids, height: int, width: int, out, 
                               int(height), int(width), pitch, _ptr(out), _stream(stream)), "vp_synth_frames")
 
 
+def dedup_clips(keys, unique_id, unique_list, n_unique, stream=None) -> None:
+    """vp_dedup_clips (N3).  keys: uint64 (or int64) device tensor [n]; outputs int32 [n], [n], [1]."""
+    check(lib.vp_dedup_clips(_ptr(keys), int(keys.numel()), _ptr(unique_id), _ptr(unique_list), _ptr(n_unique),
+                             _stream(stream)), "vp_dedup_clips")
+
+
+def dedup_views(unique_plans, unique_id, patch_offset, grid_thw, status=None, stream=None) -> None:
+    """vp_dedup_views (N3): per sample, its patch offset and grid in the unique clips' outputs."""
+    check(lib.vp_dedup_views(_ptr(unique_plans), _ptr(unique_id), int(unique_id.numel()), _ptr(patch_offset),
+                             _ptr(grid_thw), _ptr(status), _stream(stream)), "vp_dedup_views")
+
+
 # ---------------------------------------------------------------------------------------------
 # Convenience API: the whole path for a batch of clips (what a trainer calls)
 # ---------------------------------------------------------------------------------------------
@@ -218,6 +231,28 @@ class VisualPreprocessor:
         C.pointer(p)[0] = self.params
         p.launch_mask = int(pl.totals["variants"]) if pl.totals is not None else 0
         return p
+
+    def dedup(self, clips, keys, stream=None):
+        """N3: keep the first occurrence of each key.  Returns (unique clips (list), unique_list (host int list),
+        unique_id (device int32 [n]))."""
+        n = len(clips)
+        k = torch.as_tensor(np.asarray(keys, dtype=np.int64), device=self.device)
+        uid = torch.empty(max(n, 1), dtype=torch.int32, device=self.device)
+        ul = torch.empty(max(n, 1), dtype=torch.int32, device=self.device)
+        nu = torch.empty(1, dtype=torch.int32, device=self.device)
+        dedup_clips(k[:n], uid[:n], ul, nu, stream=stream)
+        u = int(nu.item())
+        ulist = ul[:u].cpu().tolist()
+        return [clips[i] for i in ulist], ulist, uid[:n]
+
+    def views(self, unique_plan: Plan, unique_id, stream=None):
+        """N3: per-sample (patch_offset into the unique pixel_values, grid_thw, status) on the device."""
+        n = unique_id.numel()
+        po = torch.empty(max(n, 1), dtype=torch.int64, device=self.device)
+        g = torch.empty(max(n, 1), 3, dtype=torch.int64, device=self.device)
+        st = torch.empty(max(n, 1), dtype=torch.int32, device=self.device)
+        dedup_views(unique_plan.plans_dev, unique_id, po[:n], g[:n], st[:n], stream=stream)
+        return po[:n], g[:n], st[:n]
 
     def alloc_outputs(self, pl: Plan):
         dt = torch.float32 if self.params.out_dtype == VP_OUT_F32 else torch.bfloat16

@@ -26,7 +26,7 @@ TOT_LEN = 12
 
 EXPORTED = ["vp_plan_frames", "vp_resize_workspace_bytes", "vp_resize_normalize_patchify", "vp_rope_index_workspace_bytes", "vp_rope_index",
             "vp_pack_offsets", "vp_plan_records", "vp_synth_frames", "vp_status_string", "vp_last_error_detail",
-            "vp_abi_version", "vp_struct_sizes"]
+            "vp_abi_version", "vp_struct_sizes", "vp_dedup_clips", "vp_dedup_views"]
 
 
 class VpParams(C.Structure):
@@ -68,6 +68,8 @@ def _load() -> C.CDLL:
         "vp_last_error_detail": (C.c_char_p, []),
         "vp_abi_version": (i32, []),
         "vp_struct_sizes": (i32, []),
+        "vp_dedup_clips": (i32, [vp, i32, vp, vp, vp, vp]),
+        "vp_dedup_views": (i32, [vp, vp, i32, vp, vp, vp, vp]),
     }
     for name, (res, args) in sig.items():
         f = getattr(lib, name)

@@ -203,3 +203,17 @@ def test_plan_invalid_clip_is_skipped():
     plans, tot = O.plan_batch(params, [I.clip(0, 30.0, 64, 64), I.clip(10, 30.0, 64, 64), I.clip(5, 0.0, 64, 64)])
     assert [p.status for p in plans] == [O.VP_EINVAL, O.VP_OK, O.VP_EINVAL]
     assert tot["n_videos"] == 1 and plans[1].grid_index == 0
+
+
+def test_dedup_keys_brute_force():
+    """N3 oracle: first occurrence kept, batch order, every sample maps to a unique clip with its own key
+    (brute force over all small key sequences)."""
+    import itertools
+    for n in range(0, 6):
+        for keys in itertools.product(range(3), repeat=n):
+            uid, ul = O.dedup_keys(list(keys))
+            assert len(uid) == n and len(set(keys)) == len(ul)
+            assert ul == sorted(ul) and all(keys[i] not in keys[:i] for i in ul)
+            assert all(keys[ul[uid[k]]] == keys[k] and ul[uid[k]] <= k for k in range(n))
+    uid, ul = O.dedup_keys([7] * 8 + [3] * 8)                      # GRPO: 2 prompts x 8 rollouts
+    assert ul == [0, 8] and uid == [0] * 8 + [1] * 8
