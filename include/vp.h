@@ -46,7 +46,11 @@ typedef enum {
   VP_EUNSUPPORTED = 6 /* a configuration beyond the kernels' envelope (merge_size*patch_size > 64) */
 } vp_status;
 
-typedef enum { VP_SAMPLE_CENTER_BIN = 0 /* S:78 (C1, C2) */ } vp_sampling;
+typedef enum { VP_SAMPLE_CENTER_BIN = 0 /* S:78 (C1, C2) */,
+               VP_SAMPLE_LINSPACE = 1   /* HF Qwen3-VL sample_frames (C1/C2 HF rule, N1): n = int(total/src_fps*fps),
+                                           clamped to [min_frames, min(max_frames, total)], no tp rounding;
+                                           idx_i = round_half_even(i * (total-1)/(n-1)), idx_{n-1} = total-1 */
+} vp_sampling;
 typedef enum { VP_BUDGET_PER_FRAME = 0 /* P:271 */, VP_BUDGET_TOTAL = 1 /* Qwen3-VL T-aware, C8 */ } vp_budget_mode;
 typedef enum { VP_ROPE_QWEN3_SPLIT = 0 /* C18 */, VP_ROPE_QWEN2 = 1 /* classic, C19 */,
                VP_ROPE_QWEN25 = 2 /* time-scaled, C19 */ } vp_rope_variant;
@@ -55,7 +59,8 @@ typedef enum { VP_SYNTH_RAMP = 0 /* S:71 */, VP_SYNTH_NOISE = 1 } vp_synth_kind;
 
 /* Preprocessing parameters (S:29-34 PreprocessParams; P:90 independent budgets; P:271 values).
  * Invariants checked on the host (VP_EINVAL): patch,merge,tp >= 1; max_frames >= tp;
- * video_max_pixels, image_max_pixels >= (patch*merge)^2; target_fps > 0; std[c] != 0. */
+ * video_max_pixels, image_max_pixels >= (patch*merge)^2; target_fps > 0; std[c] != 0; sampling in vp_sampling;
+ * 0 <= min_frames <= max_frames. */
 typedef struct {
   double  target_fps;          /* 2.0 */
   int32_t max_frames;          /* 128 */
@@ -74,7 +79,9 @@ typedef struct {
                                   of the plan (bit v = some valid clip uses kernel variant v); kernels of absent
                                   variants are not launched.  0 = unknown: launch every kernel.  Ignored by the
                                   other calls.  A mask missing a present variant leaves its clips unwritten. */
-} vp_params;                   /* 112 bytes */
+  int32_t min_frames;          /* VP_SAMPLE_LINSPACE only: lower clamp of n (HF Qwen3-VL: 4) */
+  int32_t reserved_;           /* 0 */
+} vp_params;                   /* 120 bytes */
 
 /* One input clip (S:42-47 VideoMetadata source fields).  Images: is_image=1, the frame count and
  * fps are ignored (an image is one frame, routed to the image budget and output, P:90 / P:165). */
@@ -128,6 +135,8 @@ enum {
  * vp_plan_frames -- H1-H4 + H9: frame plan, smart_resize, grid and offsets for n clips.
  *   O1: n = clamp(floor(total/src_fps*target_fps), tp, max_frames), n <= total (C3),
  *      rounded down to a multiple of tp; idx_i = min(total-1, floor((i+1/2)*total/n)).
+ *      p->sampling == VP_SAMPLE_LINSPACE: the HF Qwen3-VL rule instead (see vp_sampling; a clip whose n is 0
+ *      -- min_frames = 0 and a sub-frame duration -- is invalid).
  *   O2 (C5-C8): smart_resize under image_max_pixels (images) or video_max_pixels (videos,
  *      per-frame or total budget).  O3: grid = (ceil(n/tp), H'/p, W'/p).
  *   O10 (C22): per temporal group timestamp (idx[g*tp]/fps + idx[g*tp+tp-1]/fps)/2 after
@@ -232,6 +241,15 @@ vp_status vp_pack_offsets(const int32_t* gathered, int32_t world, int32_t clips_
  * plans (dev) [n]; records (dev) [n*4].  Invalid clips give (0,0,0,0). */
 vp_status vp_plan_records(const vp_clip_plan* plans, int32_t n, int32_t merge_size,
                           int32_t* records, void* stream);
+
+/* ---------------------------------------------------------------------------------------------
+ * vp_plan_second_per_grid -- N2 (Qwen2.5-VL time-scaled MRoPE, C19): per valid video, the seconds one temporal
+ * grid spans, second_per_grid[grid_index] = temporal_patch_size / sampled_fps with HF's sampled fps
+ * n / total * source_fps (evaluated in that f64 order, no contraction).  Feeds vp_rope_index(VP_ROPE_QWEN25).
+ * clips (dev) [n], plans (dev) [n] of the same vp_plan_frames call; second_per_grid (dev) [n_videos] f64.
+ * ------------------------------------------------------------------------------------------- */
+vp_status vp_plan_second_per_grid(const vp_clip_desc* clips, const vp_clip_plan* plans, int32_t n,
+                                  int32_t temporal_patch_size, double* second_per_grid, void* stream);
 
 /* ---------------------------------------------------------------------------------------------
  * vp_dedup_clips -- N3: hash-based deduplication of a batch ("hash-based deduplication"; GRPO n = 8 rollouts

@@ -26,11 +26,11 @@ import numpy as np
 
 __all__ = [
     "VP_OK", "VP_EINVAL", "VP_EMISMATCH",
-    "sample_frame_indices", "effective_fps", "round_half_even_div", "smart_resize",
+    "sample_frame_indices", "sample_frame_indices_hf", "effective_fps", "round_half_even_div", "smart_resize",
     "smart_resize_exact_floor", "grid_thw", "clip_budget", "plan_clip", "plan_batch",
     "keys_cubic", "aa_weights", "weight_matrix", "resize_frame", "resize_pixel",
     "normalize", "temporal_pad", "patchify", "patch_coords", "bf16_rne_bits", "bf16_bits_to_f64",
-    "group_timestamps", "second_per_grid", "qwen25_interval", "rope_index", "process_batch", "ClipPlan",
+    "group_timestamps", "hf_sampled_fps", "second_per_grid", "qwen25_interval", "rope_index", "process_batch", "ClipPlan",
     "dedup_keys",
 ]
 
@@ -58,6 +58,26 @@ def sample_frame_indices(total: int, src_fps: float, target_fps: float, max_fram
     if n >= tp:
         n = tp * (n // tp)
     idx = [min(total - 1, ((2 * i + 1) * total) // (2 * n)) for i in range(n)]
+    return n, idx
+
+
+def sample_frame_indices_hf(total: int, src_fps: float, target_fps: float, min_frames: int, max_frames: int):
+    """HF drop-in sampling (reading C1/C2, HF rule; N1): Qwen3-VL's ``sample_frames``.
+
+    n   = int(total / src_fps * target_fps)                 (f64, truncation)
+    n   = min(max(n, min_frames), max_frames, total)       (no rounding to a multiple of tp)
+    idx = round_half_even(linspace(0, total - 1, n))      (numpy linspace: i * ((total-1)/(n-1)), last = total-1)
+    Returns (n, [idx...]).  Raises ValueError on total<1, fps<=0 or n == 0."""
+    if total < 1 or not (src_fps > 0):
+        raise ValueError("invalid input: total_source_frames >= 1 and source_fps > 0 required (S:79)")
+    n = int(float(total) / float(src_fps) * float(target_fps))
+    n = min(max(n, min_frames), max_frames, total)
+    if n < 1:
+        raise ValueError("no frame sampled")
+    if n == 1:
+        return 1, [0]
+    step = float(total - 1) / float(n - 1)
+    idx = [round(i * step) for i in range(n - 1)] + [total - 1]     # Python round: half to even
     return n, idx
 
 
@@ -176,8 +196,13 @@ def plan_clip(params: dict, c: dict) -> ClipPlan:
         H, W = smart_resize(h, w, clip_budget(params, True), f, params["min_pixels"])
     else:
         try:
-            n, idx = sample_frame_indices(int(c["total_source_frames"]), float(c["source_fps"]),
-                                          float(params["target_fps"]), int(params["max_frames"]), tp)
+            if params.get("sampling", 0) == 1:
+                n, idx = sample_frame_indices_hf(int(c["total_source_frames"]), float(c["source_fps"]),
+                                                 float(params["target_fps"]), int(params.get("min_frames", 4)),
+                                                 int(params["max_frames"]))
+            else:
+                n, idx = sample_frame_indices(int(c["total_source_frames"]), float(c["source_fps"]),
+                                              float(params["target_fps"]), int(params["max_frames"]), tp)
         except ValueError:
             return ClipPlan(VP_EINVAL, is_image)
         eff = effective_fps(n, float(c["source_fps"]), int(c["total_source_frames"]))
@@ -376,6 +401,11 @@ def group_timestamps(idx, src_fps: float, tp: int):
 # ---------------------------------------------------------------------------
 # O11 -- MRoPE position ids + strict placeholder validation (C18-C24)
 # ---------------------------------------------------------------------------
+
+def hf_sampled_fps(n: int, total: int, src_fps: float) -> float:
+    """HF VideoMetadata.sampled_fps: len(indices) / total_num_frames * fps (f64, in this order)."""
+    return n / float(total) * float(src_fps)
+
 
 def second_per_grid(tp: int, sampled_fps: float) -> float:
     """Seconds spanned by one temporal grid of a video (Qwen2.5-VL, reading C19): tp / sampled fps

@@ -13,18 +13,22 @@ from dataclasses import dataclass
 import numpy as np
 import torch
 
+from .presets import PRESETS, preset
 from ._lib import (DESC_DTYPE, PLAN_DTYPE, TOT, TOT_LEN, VP_BUDGET_PER_FRAME, VP_BUDGET_TOTAL, VP_ECAPACITY,
                    VP_EINVAL, VP_EMISMATCH, VP_EUNSUPPORTED, VP_OK, VP_OUT_BF16, VP_OUT_F32, VP_ROPE_QWEN2,
-                   VP_ROPE_QWEN3_SPLIT, VP_ROPE_QWEN25, VP_SYNTH_NOISE, VP_SYNTH_RAMP, VpError, VpParams,
+                   VP_ROPE_QWEN3_SPLIT, VP_ROPE_QWEN25, VP_SAMPLE_CENTER_BIN, VP_SAMPLE_LINSPACE, VP_SYNTH_NOISE,
+                   VP_SYNTH_RAMP, VpError, VpParams,
                    check, lib)
 
 __all__ = [
     "make_params", "clip_desc_array", "plan_frames", "resize_normalize_patchify", "resize_workspace_bytes",
     "resize_workspace", "rope_index",
     "rope_index_workspace_bytes", "plan_records", "pack_offsets", "synth_frames", "dedup_clips", "dedup_views",
+    "plan_second_per_grid", "preset", "PRESETS",
     "VisualPreprocessor",
     "PlacementMismatch", "VpError", "VpParams", "DESC_DTYPE", "PLAN_DTYPE", "TOT", "TOT_LEN",
     "VP_ROPE_QWEN3_SPLIT", "VP_ROPE_QWEN2", "VP_ROPE_QWEN25", "VP_OUT_BF16", "VP_OUT_F32",
+    "VP_SAMPLE_CENTER_BIN", "VP_SAMPLE_LINSPACE",
     "VP_BUDGET_PER_FRAME", "VP_BUDGET_TOTAL", "VP_SYNTH_RAMP", "VP_SYNTH_NOISE", "VP_OK", "VP_EINVAL",
     "VP_EMISMATCH", "VP_ECAPACITY", "VP_EUNSUPPORTED", "lib",
 ]
@@ -50,13 +54,14 @@ def _stream(stream) -> int | None:
 
 def make_params(target_fps=2.0, max_frames=128, temporal_patch_size=2, patch_size=16, merge_size=2,
                 video_max_pixels=262144, image_max_pixels=1048576, min_pixels=0, budget_mode=0, sampling=0,
-                mean=(0.5, 0.5, 0.5), std=(0.5, 0.5, 0.5), out_dtype=VP_OUT_BF16) -> VpParams:
+                mean=(0.5, 0.5, 0.5), std=(0.5, 0.5, 0.5), out_dtype=VP_OUT_BF16, min_frames=None) -> VpParams:
     """vp_params (defaults = Qwen3-VL preset with the P:271 budgets)."""
     p = VpParams()
     p.target_fps, p.max_frames, p.temporal_patch_size = float(target_fps), int(max_frames), int(temporal_patch_size)
     p.patch_size, p.merge_size = int(patch_size), int(merge_size)
     p.video_max_pixels, p.image_max_pixels, p.min_pixels = int(video_max_pixels), int(image_max_pixels), int(min_pixels)
     p.budget_mode, p.sampling, p.out_dtype = int(budget_mode), int(sampling), int(out_dtype)
+    p.min_frames = min(4, p.max_frames) if min_frames is None else int(min_frames)   # HF Qwen3-VL: 4
     for c in range(3):
         p.mean[c], p.std[c] = float(mean[c]), float(std[c])
     return p
@@ -147,6 +152,12 @@ def synth_frames(kind: int, seed: int, frame_ids, height: int, width: int, out, 
                               int(height), int(width), pitch, _ptr(out), _stream(stream)), "vp_synth_frames")
 
 
+def plan_second_per_grid(clips, plans, n: int, temporal_patch_size: int, second_per_grid, stream=None) -> None:
+    """vp_plan_second_per_grid (N2, Qwen2.5-VL): f64 [n_videos] seconds per temporal grid."""
+    check(lib.vp_plan_second_per_grid(_ptr(clips), _ptr(plans), int(n), int(temporal_patch_size),
+                                      _ptr(second_per_grid), _stream(stream)), "vp_plan_second_per_grid")
+
+
 def dedup_clips(keys, unique_id, unique_list, n_unique, stream=None) -> None:
     """vp_dedup_clips (N3).  keys: uint64 (or int64) device tensor [n]; outputs int32 [n], [n], [1]."""
     check(lib.vp_dedup_clips(_ptr(keys), int(keys.numel()), _ptr(unique_id), _ptr(unique_list), _ptr(n_unique),
@@ -184,6 +195,8 @@ class VisualPreprocessor:
 
     def __init__(self, device="cuda", **params):
         self.device = torch.device(device)
+        self.rope_variant = params.pop("rope_variant", VP_ROPE_QWEN3_SPLIT)
+        self.tokens_per_second = params.pop("tokens_per_second", 0)
         self.params = make_params(**params)
         self.D = 3 * self.params.temporal_patch_size * self.params.patch_size ** 2
 
@@ -231,6 +244,19 @@ class VisualPreprocessor:
         C.pointer(p)[0] = self.params
         p.launch_mask = int(pl.totals["variants"]) if pl.totals is not None else 0
         return p
+
+    @classmethod
+    def from_preset(cls, name: str, device="cuda", **overrides):
+        """N2: a preprocessor for a model family (Qwen2-VL, Qwen2.5-VL, Qwen3-VL, Qwen3.5; see presets.py)."""
+        p, rope = preset(name, **overrides)
+        return cls(device=device, **p, **rope)
+
+    def second_per_grid(self, pl: Plan, stream=None) -> torch.Tensor:
+        """Per video of the plan (grid order), temporal_patch_size / HF sampled fps (Qwen2.5-VL time scale)."""
+        nv = int(pl.totals["n_videos"]) if pl.totals is not None else pl.n
+        out = torch.zeros(max(nv, 1), dtype=torch.float64, device=self.device)
+        plan_second_per_grid(pl.clips_dev, pl.plans_dev, pl.n, self.params.temporal_patch_size, out, stream=stream)
+        return out[:nv]
 
     def dedup(self, clips, keys, stream=None):
         """N3: keep the first occurrence of each key.  Returns (unique clips (list), unique_list (host int list),
@@ -287,8 +313,11 @@ class VisualPreprocessor:
 
     # -- H8 --
     def rope_index(self, mm_token_type, cu_seqlens, image_grid_thw, video_grid_thw,
-                   variant=VP_ROPE_QWEN3_SPLIT, second_per_grid=None, tokens_per_second=0, stream=None,
+                   variant=None, second_per_grid=None, tokens_per_second=None, stream=None,
                    strict=True):
+        """vp_rope_index for a packed batch; variant / tokens_per_second default to the preprocessor's (preset)."""
+        variant = self.rope_variant if variant is None else variant
+        tokens_per_second = self.tokens_per_second if tokens_per_second is None else tokens_per_second
         L = mm_token_type.numel()
         B = cu_seqlens.numel() - 1
         nv = video_grid_thw.shape[0] if video_grid_thw is not None else 0

@@ -15,6 +15,7 @@ LIB_PATH = os.path.join(HERE, "libvp.so")
 # vp_status
 VP_OK, VP_EINVAL, VP_EALIGN, VP_EMISMATCH, VP_ECAPACITY, VP_ECUDA, VP_EUNSUPPORTED = range(7)
 VP_ROPE_QWEN3_SPLIT, VP_ROPE_QWEN2, VP_ROPE_QWEN25 = 0, 1, 2
+VP_SAMPLE_CENTER_BIN, VP_SAMPLE_LINSPACE = 0, 1
 VP_OUT_BF16, VP_OUT_F32 = 0, 1
 VP_BUDGET_PER_FRAME, VP_BUDGET_TOTAL = 0, 1
 VP_SYNTH_RAMP, VP_SYNTH_NOISE = 0, 1
@@ -26,7 +27,8 @@ TOT_LEN = 12
 
 EXPORTED = ["vp_plan_frames", "vp_resize_workspace_bytes", "vp_resize_normalize_patchify", "vp_rope_index_workspace_bytes", "vp_rope_index",
             "vp_pack_offsets", "vp_plan_records", "vp_synth_frames", "vp_status_string", "vp_last_error_detail",
-            "vp_abi_version", "vp_struct_sizes", "vp_dedup_clips", "vp_dedup_views"]
+            "vp_abi_version", "vp_struct_sizes", "vp_dedup_clips", "vp_dedup_views",
+            "vp_plan_second_per_grid"]
 
 
 class VpParams(C.Structure):
@@ -34,7 +36,8 @@ class VpParams(C.Structure):
                 ("patch_size", C.c_int32), ("merge_size", C.c_int32), ("video_max_pixels", C.c_int64),
                 ("image_max_pixels", C.c_int64), ("min_pixels", C.c_int64), ("budget_mode", C.c_int32),
                 ("sampling", C.c_int32), ("mean", C.c_double * 3), ("std", C.c_double * 3),
-                ("out_dtype", C.c_int32), ("launch_mask", C.c_int32)]
+                ("out_dtype", C.c_int32), ("launch_mask", C.c_int32),
+                ("min_frames", C.c_int32), ("reserved_", C.c_int32)]
 
 
 DESC_DTYPE = np.dtype([("total_source_frames", "<i8"), ("source_fps", "<f8"), ("height", "<i4"),
@@ -70,6 +73,7 @@ def _load() -> C.CDLL:
         "vp_struct_sizes": (i32, []),
         "vp_dedup_clips": (i32, [vp, i32, vp, vp, vp, vp]),
         "vp_dedup_views": (i32, [vp, vp, i32, vp, vp, vp, vp]),
+        "vp_plan_second_per_grid": (i32, [vp, vp, i32, i32, vp, vp]),
     }
     for name, (res, args) in sig.items():
         f = getattr(lib, name)

@@ -36,8 +36,9 @@ vp_status check_params(const vp_params* p) {
     return VP_EINVAL;
   }
   if (!(p->target_fps > 0.0) || p->min_pixels < 0 || (p->budget_mode != 0 && p->budget_mode != 1) ||
-      p->sampling != 0 || (p->out_dtype != 0 && p->out_dtype != 1)) {
-    set_error("params: invalid target_fps / min_pixels / budget_mode / sampling / out_dtype");
+      (p->sampling != VP_SAMPLE_CENTER_BIN && p->sampling != VP_SAMPLE_LINSPACE) ||
+      (p->out_dtype != 0 && p->out_dtype != 1) || p->min_frames < 0 || p->min_frames > p->max_frames) {
+    set_error("params: invalid target_fps / min_pixels / budget_mode / sampling / out_dtype / min_frames");
     return VP_EINVAL;
   }
   for (int c = 0; c < 3; ++c)
@@ -127,10 +128,35 @@ __global__ void __launch_bounds__(1024) pack_kernel(const int32_t* __restrict__ 
     pat[total] = carry[1];
   }
 }
+// N2 (Qwen2.5-VL time-scaled MRoPE): per video, second_per_grid_ts = temporal_patch_size / sampled_fps with HF's
+// sampled fps n / total * src_fps (X: Qwen2_5_VLProcessor, VideoMetadata.sampled_fps), in that f64 order.
+__global__ void spg_kernel(const vp_clip_desc* __restrict__ clips, const vp_clip_plan* __restrict__ plans, int n,
+                           int tp, double* __restrict__ spg) {
+  for (int k = blockIdx.x * blockDim.x + threadIdx.x; k < n; k += gridDim.x * blockDim.x) {
+    const vp_clip_plan pl = plans[k];
+    if (pl.status != VP_OK || pl.is_image) continue;
+    const double sampled = __dmul_rn(__ddiv_rn((double)pl.n_frames, (double)clips[k].total_source_frames),
+                                     clips[k].source_fps);
+    spg[pl.grid_index] = __ddiv_rn((double)tp, sampled);
+  }
+}
 }  // namespace
 }  // namespace vp
 
 extern "C" {
+
+vp_status vp_plan_second_per_grid(const vp_clip_desc* clips, const vp_clip_plan* plans, int32_t n,
+                                  int32_t temporal_patch_size, double* second_per_grid, void* stream) {
+  if (n < 0 || temporal_patch_size < 1 || (n > 0 && (clips == nullptr || plans == nullptr ||
+                                                      second_per_grid == nullptr))) {
+    vp::set_error("vp_plan_second_per_grid: invalid arguments");
+    return VP_EINVAL;
+  }
+  if (n == 0) return VP_OK;
+  vp::spg_kernel<<<(n + 255) / 256, 256, 0, vp::as_stream(stream)>>>(clips, plans, n, temporal_patch_size,
+                                                                     second_per_grid);
+  return vp::launch_status("vp_plan_second_per_grid");
+}
 
 const char* vp_status_string(vp_status s) {
   switch (s) {

@@ -60,12 +60,22 @@ __device__ ClipResult plan_one(const vp_params& P, const vp_clip_desc& c) {
     // O1 (S:78 + C3): d = floor((total / src_fps) * target_fps)
     if (c.total_source_frames < 1 || !(c.source_fps > 0.0)) return r;
     double d = floor(__dmul_rn(__ddiv_rn((double)c.total_source_frames, c.source_fps), P.target_fps));
-    if (d < (double)tp) n = tp;
-    else if (d > (double)P.max_frames) n = P.max_frames;
-    else n = (int64_t)d;
-    n = min(n, (int64_t)P.max_frames);
-    n = min(n, c.total_source_frames);
-    if (n >= tp) n = tp * (n / tp);
+    if (P.sampling == VP_SAMPLE_LINSPACE) {
+      // HF Qwen3-VL sample_frames: int(total / fps * target), min(max(n, min_frames), max_frames, total)
+      if (d < (double)P.min_frames) n = P.min_frames;
+      else if (d > (double)P.max_frames) n = P.max_frames;
+      else n = (int64_t)d;
+      n = min(n, (int64_t)P.max_frames);
+      n = min(n, c.total_source_frames);
+      if (n < 1) return r;
+    } else {
+      if (d < (double)tp) n = tp;
+      else if (d > (double)P.max_frames) n = P.max_frames;
+      else n = (int64_t)d;
+      n = min(n, (int64_t)P.max_frames);
+      n = min(n, c.total_source_frames);
+      if (n >= tp) n = tp * (n / tp);
+    }
     r.total = c.total_source_frames;
     r.src_fps = c.source_fps;
     // C23: effective fps = n*src_fps/total
@@ -81,6 +91,15 @@ __device__ ClipResult plan_one(const vp_params& P, const vp_clip_desc& c) {
   return r;
 }
 
+// HF linspace index: numpy linspace(0, total-1, n)[i] = i * ((total-1)/(n-1)) in f64 (last = total-1 exactly,
+// n = 1 -> 0), rounded half to even (np.round).
+__device__ __forceinline__ int64_t linspace_index(int64_t i, int64_t total, int64_t n) {
+  if (n <= 1) return 0;
+  if (i == n - 1) return total - 1;
+  const double step = __ddiv_rn((double)(total - 1), (double)(n - 1));
+  return (int64_t)rint(__dmul_rn((double)i, step));
+}
+
 // Center-of-bin index: min(total-1, floor((2i+1)*total / (2n))) in exact integers.
 __device__ __forceinline__ int64_t frame_index(int64_t i, int64_t total, int64_t n) {
   const uint64_t a = (uint64_t)(2 * i + 1), t = (uint64_t)total;
@@ -92,6 +111,10 @@ __device__ __forceinline__ int64_t frame_index(int64_t i, int64_t total, int64_t
     q = (int64_t)(num / (unsigned __int128)(2 * n));
   }
   return q < total - 1 ? q : total - 1;
+}
+
+__device__ __forceinline__ int64_t sample_index(int sampling, int64_t i, int64_t total, int64_t n) {
+  return sampling == VP_SAMPLE_LINSPACE ? linspace_index(i, total, n) : frame_index(i, total, n);
 }
 
 __global__ void __launch_bounds__(kPlanThreads, 1)
@@ -220,7 +243,8 @@ plan_kernel(vp_params P, const vp_clip_desc* __restrict__ clips, int n, vp_clip_
 //      integer divisions dominate K1 for long clips, so they are spread over the whole GPU) ----
 constexpr int kFillThreads = 256;
 __global__ void __launch_bounds__(kFillThreads)
-plan_fill_kernel(int64_t tp, const vp_clip_desc* __restrict__ clips, int n, const vp_clip_plan* __restrict__ plans,
+plan_fill_kernel(int64_t tp, int sampling, const vp_clip_desc* __restrict__ clips, int n,
+                 const vp_clip_plan* __restrict__ plans,
                  int64_t* __restrict__ frame_indices, int64_t index_cap, double* __restrict__ ts, int64_t ts_cap,
                  int64_t* __restrict__ totals) {
   const int lane = threadIdx.x & 31;
@@ -238,7 +262,7 @@ plan_fill_kernel(int64_t tp, const vp_clip_desc* __restrict__ clips, int n, cons
   } else {
     const int64_t total = clips[c].total_source_frames;
     for (int64_t i = lane; i < nn; i += 32) {
-      if (off + i < index_cap) frame_indices[off + i] = frame_index(i, total, nn);
+      if (off + i < index_cap) frame_indices[off + i] = sample_index(sampling, i, total, nn);
       else flags |= 1ull;
     }
     if (ts != nullptr) {
@@ -246,8 +270,8 @@ plan_fill_kernel(int64_t tp, const vp_clip_desc* __restrict__ clips, int n, cons
       const int64_t groups = ceil_div(nn, tp);
       for (int64_t g = lane; g < groups; g += 32) {
         int64_t i0 = g * tp, i1 = min(g * tp + tp - 1, nn - 1);   // pad with last index (C22)
-        double a = __ddiv_rn((double)frame_index(i0, total, nn), fps);
-        double b = __ddiv_rn((double)frame_index(i1, total, nn), fps);
+        double a = __ddiv_rn((double)sample_index(sampling, i0, total, nn), fps);
+        double b = __ddiv_rn((double)sample_index(sampling, i1, total, nn), fps);
         const int64_t o = pl.group_offset + g;
         if (o < ts_cap) ts[o] = __dmul_rn(__dadd_rn(a, b), 0.5);
         else flags |= 2ull;
@@ -281,7 +305,8 @@ extern "C" vp_status vp_plan_frames(const vp_params* p, const vp_clip_desc* clip
   if (n > 0) {
     const int per = vp::kFillThreads / 32;
     vp::plan_fill_kernel<<<(n + per - 1) / per, vp::kFillThreads, 0, vp::as_stream(stream)>>>(
-        p->temporal_patch_size, clips, n, plans, frame_indices, index_cap, group_timestamps, ts_cap, totals);
+        p->temporal_patch_size, p->sampling, clips, n, plans, frame_indices, index_cap, group_timestamps, ts_cap,
+        totals);
   }
   return vp::launch_status("vp_plan_frames");
 }

@@ -17,7 +17,8 @@ def oracle_params(vp_params) -> dict:
     return dict(target_fps=p.target_fps, max_frames=p.max_frames, temporal_patch_size=p.temporal_patch_size,
                 patch_size=p.patch_size, merge_size=p.merge_size, video_max_pixels=p.video_max_pixels,
                 image_max_pixels=p.image_max_pixels, min_pixels=p.min_pixels, budget_mode=p.budget_mode,
-                sampling=p.sampling, mean=tuple(p.mean), std=tuple(p.std), out_dtype=p.out_dtype)
+                sampling=p.sampling, mean=tuple(p.mean), std=tuple(p.std), out_dtype=p.out_dtype,
+                min_frames=p.min_frames)
 
 
 def _ord_bf16(bits: np.ndarray) -> np.ndarray:

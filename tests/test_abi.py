@@ -38,7 +38,7 @@ def test_binding_loads_and_struct_sizes_match():
     from paper_2604_16893_b200 import _lib
     assert set(_declared_symbols()) == set(_lib.EXPORTED)
     assert vp.lib.vp_abi_version() == 1
-    assert C.sizeof(vp.VpParams) == 112 and vp.DESC_DTYPE.itemsize == 32 and vp.PLAN_DTYPE.itemsize == 104
+    assert C.sizeof(vp.VpParams) == 120 and vp.DESC_DTYPE.itemsize == 32 and vp.PLAN_DTYPE.itemsize == 104
 
 
 def test_host_side_errors_are_synchronous():

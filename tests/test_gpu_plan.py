@@ -101,3 +101,15 @@ def test_plan_empty_and_overflow_flags():
     vp.plan_frames(pre.params, desc, 1, plans, idx, tot)
     assert tot[vp.TOT["flags"]].item() & 1
     assert (idx.cpu() >= 0).all()
+
+
+@pytest.mark.parametrize("seed", range(4))
+def test_plan_hf_linspace_sampling(seed):
+    """N1 sampling (VP_SAMPLE_LINSPACE, HF Qwen3-VL sample_frames): n, indices, effective fps and timestamps
+    bit-exact vs the oracle (itself pinned to HF in tests/test_oracle_plan.py), incl. n not a multiple of tp
+    (temporal pad), n < min_frames clamps, total < min_frames, and min_frames = 0 with sub-frame durations."""
+    rng = random.Random(40 + seed)
+    kw = dict(target_fps=rng.choice([0.5, 1.0, 2.0, 4.0]), max_frames=rng.choice([16, 64, 768]),
+              temporal_patch_size=rng.choice([1, 2, 3]), patch_size=16, merge_size=2,
+              video_max_pixels=262144, image_max_pixels=1048576, sampling=1, min_frames=rng.choice([0, 1, 4]))
+    _compare(kw, _random_clips(rng, rng.choice([37, 600, 1500])))

@@ -121,3 +121,45 @@ def test_fuzz_with_adversarial_mismatches(seed):
         if rng.random() < 0.1 and img:
             img.pop()                                        # a run without a grid
         _compare(seqs, img, vid, m)
+
+
+@pytest.mark.parametrize("name", ["qwen2_vl", "qwen2_5_vl", "qwen3_vl", "qwen3_5"])
+def test_presets_end_to_end(name):
+    """N2: each family preset through plan -> (Qwen2.5: vp_plan_second_per_grid) -> MRoPE, vs the oracle; the
+    per-video seconds per grid bit-exact with the oracle's HF-order sampled fps."""
+    import paper_2604_16893_b200 as vp
+    pre = vp.VisualPreprocessor.from_preset(name, max_frames=16, video_max_pixels=50176)
+    clips = [I.clip(300, 29.97, 360, 640), I.image(300, 400), I.clip(50, 10.0, 224, 224), I.clip(7, 2.0, 100, 90),
+             I.clip(1000, 59.94, 480, 854)]
+    pl = pre.plan(clips)
+    from parity import oracle_params
+    op = oracle_params(pre.params)
+    oplans, _ = O.plan_batch(op, clips)
+    m = op["merge_size"]
+    spg = pre.second_per_grid(pl).cpu().tolist()
+    ref_spg = [O.second_per_grid(op["temporal_patch_size"], O.hf_sampled_fps(o.n, c["total_source_frames"],
+                                                                             c["source_fps"]))
+               for o, c in zip(oplans, clips) if not o.is_image]
+    assert spg == ref_spg
+    seqs, ig, vg = [], [], []
+    for o in oplans:
+        if o.is_image:
+            seqs.append(I.token_types([(0, 3), (1, o.tokens), (0, 2)]))
+            ig.append(o.grid)
+        else:
+            vg.append(o.grid)
+            if pre.rope_variant == vp.VP_ROPE_QWEN3_SPLIT:
+                runs = [(0, 4)]
+                for _ in range(o.grid[0]):
+                    runs += [(0, 7), (2, o.grid[1] * o.grid[2] // m ** 2), (0, 1)]
+            else:
+                runs = [(0, 4), (2, o.tokens), (0, 3)]
+            seqs.append(I.token_types(runs))
+    tt = torch.from_numpy(np.concatenate(seqs)).cuda()
+    cu = torch.tensor(np.concatenate([[0], np.cumsum([len(s) for s in seqs])]), dtype=torch.int64).cuda()
+    igt = torch.tensor(ig, dtype=torch.int64).cuda()
+    vgt = torch.tensor(vg, dtype=torch.int64).cuda()
+    pos, deltas, st = pre.rope_index(tt, cu, igt, vgt, second_per_grid=pre.second_per_grid(pl))
+    ids, od, ost, bst = O.rope_index(seqs, ig, vg, m, variant=pre.rope_variant, second_per_grid_ts=ref_spg,
+                                     tokens_per_second=pre.tokens_per_second)
+    assert np.array_equal(pos.cpu().numpy(), np.concatenate(ids, axis=1)) and deltas.cpu().tolist() == od

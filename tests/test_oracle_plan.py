@@ -217,3 +217,20 @@ def test_dedup_keys_brute_force():
             assert all(keys[ul[uid[k]]] == keys[k] and ul[uid[k]] <= k for k in range(n))
     uid, ul = O.dedup_keys([7] * 8 + [3] * 8)                      # GRPO: 2 prompts x 8 rollouts
     assert ul == [0, 8] and uid == [0] * 8 + [1] * 8
+
+
+def test_hf_sampling_matches_hf_processor():
+    """N1 oracle pin: sample_frame_indices_hf == HF Qwen3VLVideoProcessor.sample_frames (default fps 2, min 4,
+    max 768) over random and edge metadata (total < 4, exact halves of linspace, long videos)."""
+    import random
+    from transformers.models.qwen3_vl.video_processing_qwen3_vl import Qwen3VLVideoProcessor
+    from transformers.video_utils import VideoMetadata
+    proc = Qwen3VLVideoProcessor()
+    rng = random.Random(3)
+    cases = [(1, 30.0), (2, 30.0), (3, 1.0), (7, 2.0), (100, 10.0), (1800, 30.0), (108000, 30.0), (13, 2.0),
+             (61, 23.976)] + [(rng.randint(1, 50000), rng.choice([1.0, 24.0, 29.97, 30.0, 60.0, rng.uniform(0.3, 120)]))
+                              for _ in range(400)]
+    for total, fps in cases:
+        ref = proc.sample_frames(VideoMetadata(total_num_frames=total, fps=fps))
+        n, idx = O.sample_frame_indices_hf(total, fps, proc.fps, proc.min_frames, proc.max_frames)
+        assert list(ref) == idx and n == len(ref), (total, fps)
