@@ -271,6 +271,29 @@ vp_status vp_dedup_views(const vp_clip_plan* unique_plans, const int32_t* unique
                          int64_t* patch_offset, int64_t* grid_thw, int32_t* status, void* stream);
 
 /* ---------------------------------------------------------------------------------------------
+ * vp_nv12_to_rgb -- N4 upstream: NVDEC-style NV12 frames (Y plane, then an interleaved U,V plane of height/2 rows,
+ * 4:2:0, each 2x2 block sharing one U,V pair) -> u8 RGB THWC, BT.601 limited range in OpenCV's fixed-point form
+ * (COLOR_YUV2RGB_NV12): y' = max(0, Y-16)*1220542, R = sat((y' + 2^19 + 1673527*(V-128)) >> 20),
+ * G = sat((y' + 2^19 - 852492*(V-128) - 409993*(U-128)) >> 20), B = sat((y' + 2^19 + 2116026*(U-128)) >> 20).
+ * P:73 ("decodes, resamples, and resizes"): the decoder output feeds K3 without a host round trip.
+ *   y, uv (dev): frame f's planes at y + f*frame_stride and uv + f*frame_stride, rows `pitch` bytes apart;
+ *   rgb (dev): frame f row r at rgb + f*rgb_frame_stride + r*rgb_pitch (e.g. a clip's slot in the K3 frame buffer).
+ *   height, width even, >= 2.  Errors: VP_EINVAL, VP_ECUDA.
+ *
+ * vp_vision_ids -- N4 downstream: for the vision tower, per pixel_values row (O8 order) of every grid in
+ * grid_thw (dev) [n_grids,3]: pos_ids (dev) [sum t*h*w, 2] int32 = (hb*m + mh, wb*m + mw) (its patch's row and
+ * column in the frame); cu_seqlens (dev) [sum t + 1] int32 = 0 then the cumulative patch count at the end of every
+ * temporal patch (X: HF Qwen3-VL vision model rot_pos_emb and cu_seqlens).  workspace (dev)
+ * vp_vision_ids_workspace_bytes(n_grids) bytes, 8-B aligned.  Errors: VP_EINVAL, VP_ECUDA.
+ * ------------------------------------------------------------------------------------------- */
+vp_status vp_nv12_to_rgb(const uint8_t* y, const uint8_t* uv, int64_t pitch, int64_t frame_stride, int32_t height,
+                         int32_t width, int32_t n_frames, uint8_t* rgb, int64_t rgb_pitch, int64_t rgb_frame_stride,
+                         void* stream);
+size_t vp_vision_ids_workspace_bytes(int32_t n_grids);
+vp_status vp_vision_ids(const int64_t* grid_thw, int32_t n_grids, int32_t merge_size, int32_t* pos_ids,
+                        int32_t* cu_seqlens, void* workspace, size_t workspace_bytes, void* stream);
+
+/* ---------------------------------------------------------------------------------------------
  * vp_synth_frames -- test/bench input generator (not part of the hot path; never timed).
  *   RAMP: (seed*2654435761 + i*97 + y*31 + x*7 + c) mod 256, i = frame_ids[f]
  *   NOISE : top 8 bits of splitmix64(((i*H + y)*W + x)*3 + c + seed*0xD1B54A32D192ED03)

@@ -31,7 +31,7 @@ __all__ = [
     "keys_cubic", "aa_weights", "weight_matrix", "resize_frame", "resize_pixel",
     "normalize", "temporal_pad", "patchify", "patch_coords", "bf16_rne_bits", "bf16_bits_to_f64",
     "group_timestamps", "hf_sampled_fps", "second_per_grid", "qwen25_interval", "rope_index", "process_batch", "ClipPlan",
-    "dedup_keys",
+    "dedup_keys", "nv12_to_rgb", "vision_pos_ids", "vision_cu_seqlens",
 ]
 
 VP_OK, VP_EINVAL, VP_EMISMATCH = 0, 1, 3
@@ -527,3 +527,49 @@ def dedup_keys(keys):
             unique_list.append(k)
         unique_id.append(first[key])
     return unique_id, unique_list
+
+
+# ---------------------------------------------------------------------------
+# N4 -- adjacent steps: NVDEC NV12 -> RGB upstream, vision-tower patch ids downstream
+# ---------------------------------------------------------------------------
+
+def nv12_to_rgb(y_plane: np.ndarray, uv_plane: np.ndarray) -> np.ndarray:
+    """BT.601 limited-range YCbCr -> RGB in OpenCV's fixed-point form (COLOR_YUV2RGB_NV12; coefficients x 2^20:
+    1.164 -> 1220542, 1.596 -> 1673527, -0.813 -> -852492, -0.391 -> -409993, 2.018 -> 2116026), chroma shared by
+    each 2x2 block.  y_plane u8 [H, W], uv_plane u8 [H/2, W] (U, V interleaved).  Plain integer loops per pixel."""
+    H, W = y_plane.shape
+    out = np.zeros((H, W, 3), dtype=np.uint8)
+    sat = lambda v: 0 if v < 0 else (255 if v > 255 else v)
+    for r in range(H):
+        for c in range(W):
+            u = int(uv_plane[r // 2, 2 * (c // 2)]) - 128
+            v = int(uv_plane[r // 2, 2 * (c // 2) + 1]) - 128
+            yy = max(0, int(y_plane[r, c]) - 16) * 1220542
+            half = 1 << 19
+            out[r, c, 0] = sat((yy + half + 1673527 * v) >> 20)
+            out[r, c, 1] = sat((yy + half - 852492 * v - 409993 * u) >> 20)
+            out[r, c, 2] = sat((yy + half + 2116026 * u) >> 20)
+    return out
+
+
+def vision_pos_ids(grids, merge: int) -> np.ndarray:
+    """Per pixel_values row of every (t, h, w) grid (O8 order: frame, merge-row block, merge-column block, mh, mw),
+    the patch's (row, col) in its frame: (hb*m + mh, wb*m + mw)  (X: HF Qwen3-VL vision rot_pos_emb)."""
+    ids = []
+    for t, h, w in grids:
+        for _ in range(t):
+            for hb in range(h // merge):
+                for wb in range(w // merge):
+                    for mh in range(merge):
+                        for mw in range(merge):
+                            ids.append((hb * merge + mh, wb * merge + mw))
+    return np.array(ids, dtype=np.int64).reshape(-1, 2)
+
+
+def vision_cu_seqlens(grids) -> list:
+    """0, then the cumulative patch count at the end of every temporal patch (frame) of every grid."""
+    cu = [0]
+    for t, h, w in grids:
+        for _ in range(t):
+            cu.append(cu[-1] + h * w)
+    return cu

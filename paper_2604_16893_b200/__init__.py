@@ -24,7 +24,7 @@ __all__ = [
     "make_params", "clip_desc_array", "plan_frames", "resize_normalize_patchify", "resize_workspace_bytes",
     "resize_workspace", "rope_index",
     "rope_index_workspace_bytes", "plan_records", "pack_offsets", "synth_frames", "dedup_clips", "dedup_views",
-    "plan_second_per_grid", "preset", "PRESETS",
+    "plan_second_per_grid", "preset", "PRESETS", "nv12_to_rgb", "vision_ids",
     "VisualPreprocessor",
     "PlacementMismatch", "VpError", "VpParams", "DESC_DTYPE", "PLAN_DTYPE", "TOT", "TOT_LEN",
     "VP_ROPE_QWEN3_SPLIT", "VP_ROPE_QWEN2", "VP_ROPE_QWEN25", "VP_OUT_BF16", "VP_OUT_F32",
@@ -156,6 +156,30 @@ def plan_second_per_grid(clips, plans, n: int, temporal_patch_size: int, second_
     """vp_plan_second_per_grid (N2, Qwen2.5-VL): f64 [n_videos] seconds per temporal grid."""
     check(lib.vp_plan_second_per_grid(_ptr(clips), _ptr(plans), int(n), int(temporal_patch_size),
                                       _ptr(second_per_grid), _stream(stream)), "vp_plan_second_per_grid")
+
+
+def nv12_to_rgb(y, uv, pitch: int, frame_stride: int, height: int, width: int, n_frames: int, rgb, rgb_pitch: int,
+                rgb_frame_stride: int, stream=None) -> None:
+    """vp_nv12_to_rgb (N4): NVDEC NV12 planes -> u8 RGB THWC frames (BT.601 limited, OpenCV fixed point).
+    y / uv / rgb may be uint8 tensors or (tensor, byte offset) views; pointers are taken from them as given."""
+    check(lib.vp_nv12_to_rgb(_ptr(y), _ptr(uv), int(pitch), int(frame_stride), int(height), int(width),
+                             int(n_frames), _ptr(rgb), int(rgb_pitch), int(rgb_frame_stride), _stream(stream)),
+          "vp_nv12_to_rgb")
+
+
+def vision_ids(grid_thw, merge_size: int, stream=None):
+    """vp_vision_ids (N4): per pixel_values row its (row, col) patch ids [P,2] int32 and cu_seqlens [sum t + 1]."""
+    g = grid_thw.contiguous()
+    n = g.shape[0]
+    gl = g.cpu().tolist()
+    P = sum(t * h * w for t, h, w in gl)
+    T = sum(t for t, _, _ in gl)
+    pos = torch.empty(max(P, 1), 2, dtype=torch.int32, device=g.device)
+    cu = torch.empty(T + 1, dtype=torch.int32, device=g.device)
+    ws = torch.empty(int(lib.vp_vision_ids_workspace_bytes(n)), dtype=torch.uint8, device=g.device)
+    check(lib.vp_vision_ids(_ptr(g), int(n), int(merge_size), _ptr(pos), _ptr(cu), _ptr(ws), ws.numel(),
+                            _stream(stream)), "vp_vision_ids")
+    return pos[:P], cu
 
 
 def dedup_clips(keys, unique_id, unique_list, n_unique, stream=None) -> None:

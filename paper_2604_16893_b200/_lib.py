@@ -28,7 +28,7 @@ TOT_LEN = 12
 EXPORTED = ["vp_plan_frames", "vp_resize_workspace_bytes", "vp_resize_normalize_patchify", "vp_rope_index_workspace_bytes", "vp_rope_index",
             "vp_pack_offsets", "vp_plan_records", "vp_synth_frames", "vp_status_string", "vp_last_error_detail",
             "vp_abi_version", "vp_struct_sizes", "vp_dedup_clips", "vp_dedup_views",
-            "vp_plan_second_per_grid"]
+            "vp_plan_second_per_grid", "vp_nv12_to_rgb", "vp_vision_ids_workspace_bytes", "vp_vision_ids"]
 
 
 class VpParams(C.Structure):
@@ -74,6 +74,9 @@ def _load() -> C.CDLL:
         "vp_dedup_clips": (i32, [vp, i32, vp, vp, vp, vp]),
         "vp_dedup_views": (i32, [vp, vp, i32, vp, vp, vp, vp]),
         "vp_plan_second_per_grid": (i32, [vp, vp, i32, i32, vp, vp]),
+        "vp_nv12_to_rgb": (i32, [vp, vp, i64, i64, i32, i32, i32, vp, i64, i64, vp]),
+        "vp_vision_ids_workspace_bytes": (sz, [i32]),
+        "vp_vision_ids": (i32, [vp, i32, i32, vp, vp, vp, sz, vp]),
     }
     for name, (res, args) in sig.items():
         f = getattr(lib, name)

@@ -15,6 +15,7 @@ cudaError_t launch_resize_fast(const vp_params* p, const vp_clip_plan* plans, in
                                int64_t vcap, cudaStream_t s);
 vp_status check_params(const vp_params* p);
 vp_status launch_status(const char* what);
+int device_sms(int dev);    // cached SM count per device (vp_resize_team.cu)
 
 inline cudaStream_t as_stream(void* s) { return reinterpret_cast<cudaStream_t>(s); }
 
