@@ -263,13 +263,82 @@ def run_ours(args, rank, world, local_rank):
     return result
 
 
+SIDE_CONFIGS = ("cfg1", "cfg2", "cfg3", "cfg4", "res480p", "res1080p", "res1440p", "res2160p")
+
+
+def measure_side(name: str, dev, steps: int = 10, warmup: int = 3):
+    """One BASELINE config (cfg1-cfg4) or source resolution (16 clips at the cfg2 budget) through K1 + K3 + K4 on
+    rank 0: ms per step, visual tokens/s, K3 event time and its HBM fraction, the kernel variants it took."""
+    import torch
+    import paper_2604_16893_b200 as vp
+    import vp_inputs as I
+    params, clips = I.config(name)
+    pre = vp.VisualPreprocessor(device=dev, **params)
+    pl = pre.plan(clips)
+    P = pre.launch_params(pl)
+    ph = pl.plans_host
+    off, pitch, total = pre.frames_layout(pl)
+    frames = torch.empty(max(total, 16), dtype=torch.uint8, device=dev)
+    idx = pl.frame_indices.cpu().numpy()
+    for k in range(pl.n):
+        n = int(ph["n_frames"][k])
+        ids = torch.from_numpy(idx[ph["index_offset"][k]: ph["index_offset"][k] + n].copy()).to(dev)
+        vp.synth_frames(vp.VP_SYNTH_NOISE, 7919 * k + 1, ids, int(ph["in_h"][k]), int(ph["in_w"][k]),
+                        frames[int(off[k]):], int(pitch[k]))
+    off_d, pitch_d = torch.from_numpy(off).to(dev), torch.from_numpy(pitch).to(dev)
+    out = pre.alloc_outputs(pl)
+    n_img = int(pl.totals["n_images"])
+    stream = torch.cuda.current_stream(dev)
+    ev = []
+
+    def step(rec=False):
+        vp.plan_frames(P, pl.clips_dev, pl.n, pl.plans_dev, pl.frame_indices, pl.totals_dev, pl.group_timestamps)
+        a = torch.cuda.Event(enable_timing=True)
+        b = torch.cuda.Event(enable_timing=True)
+        a.record(stream)
+        vp.resize_normalize_patchify(P, pl.plans_dev, pl.n, frames, off_d, pitch_d,
+                                     out["pixel_values"] if n_img else None,
+                                     out["pixel_values_videos"] if pl.totals["vid_rows"] else None,
+                                     out["image_grid_thw"], out["video_grid_thw"], out["clip_status"],
+                                     workspace=out["workspace"])
+        b.record(stream)
+        if rec:
+            ev.append((a, b))
+
+    for _ in range(warmup):
+        step()
+    torch.cuda.synchronize()
+    assert (out["clip_status"][: pl.n].cpu().numpy() == 0).all()
+    t0 = torch.cuda.Event(enable_timing=True)
+    t1 = torch.cuda.Event(enable_timing=True)
+    t0.record(stream)
+    for _ in range(steps):
+        step(True)
+    t1.record(stream)
+    torch.cuda.synchronize()
+    ms = t0.elapsed_time(t1) / steps
+    k3 = float(np.mean([a.elapsed_time(b) for a, b in ev]))
+    in_b = sum(int(ph["n_frames"][k]) * int(ph["in_h"][k]) * 3 * int(ph["in_w"][k]) for k in range(pl.n)
+               if ph["status"][k] == 0)
+    out_b = (pl.totals["vid_rows"] + pl.totals["img_rows"]) * pre.D * 2
+    peak, _ = peaks()
+    tokens = pl.totals["vid_tokens"] + pl.totals["img_tokens"]
+    res = {"ms_per_step": ms, "tokens_per_s": tokens / (ms * 1e-3), "k3_ms": k3,
+           "k3_gbs": (in_b + out_b) / (k3 * 1e-3) / 1e9, "k3_frac": (in_b + out_b) / (k3 * 1e-3) / 1e9 / peak,
+           "clips": pl.n, "src": f"{int(ph['in_h'][-1])}x{int(ph['in_w'][-1])}->{int(ph['out_h'][-1])}x{int(ph['out_w'][-1])}",
+           "variants": sorted({int(v) for v in ph["kernel_variant"][: pl.n]})}
+    del frames, out
+    torch.cuda.empty_cache()
+    return res
+
+
 def k3_launches(mask: int, n: int) -> int:
     """Kernels one vp_resize_normalize_patchify call launches for a plan whose kernel-variant mask is `mask`
     (mirrors the dispatch in vp_resize.cu): grids + generic always; the work index when any TMA variant is present;
     the team tables when team/wide clips are; one launch per present TMA variant; the direct kernel if needed."""
     has = lambda v: (mask >> v) & 1
-    tma = [has(v) for v in (0, 1, 2, 4, 5, 6)]          # mild, medium, strong, copy, team, wide
-    n_l = 2 + (1 if any(tma) else 0) + sum(tma) + (1 if (has(5) or has(6)) else 0) + has(7)
+    tma = [has(v) for v in (0, 1, 2, 4, 5, 6, 8)]       # mild, medium, strong, copy, team, wide, team-large
+    n_l = 2 + (1 if any(tma) else 0) + sum(tma) + (1 if (has(5) or has(6) or has(8)) else 0) + has(7)
     return n_l if n > 0 else 0
 
 
@@ -507,6 +576,7 @@ def main():
     ap.add_argument("--e2e-chunk", type=int, default=8)
     ap.add_argument("--no-cpu-baseline", action="store_true")
     ap.add_argument("--no-dedup", action="store_true", help="skip the 64 x 8 GRPO dedup line (N3)")
+    ap.add_argument("--no-side", action="store_true", help="skip the cfg1-cfg4 / resolution side lines")
     ap.add_argument("--cpu-clips", type=int, default=4)
     ap.add_argument("--ref-groups", type=int, default=2)
     ap.add_argument("--backend", default="nccl", choices=["nccl", "gloo"],
@@ -542,6 +612,10 @@ def main():
         nccl_glob = os.environ["NCCL_DEBUG_FILE"].replace("%h", "*").replace("%p", str(os.getpid()))
         dist.init_process_group(args.backend, device_id=torch.device("cuda", local_rank))
     res = run_ours(args, rank, world, local_rank)
+    if rank == 0 and world == 1 and not args.no_side and args.config == "cfg5":
+        # side lines: the other BASELINE configs and source resolutions (after the cfg5 buffers are released)
+        torch.cuda.empty_cache()
+        res["side_lines"] = {name: measure_side(name, torch.device("cuda", local_rank)) for name in SIDE_CONFIGS}
     if rank == 0:
         if world == 1 and not args.no_cpu_baseline:
             res["cpu_baseline"] = cpu_baseline(args.cpu_clips)

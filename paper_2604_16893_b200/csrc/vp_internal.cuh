@@ -51,7 +51,8 @@ constexpr int kTotLen = VP_TOT_LEN;
 // KV_GENERIC covers everything else (vp_resize.cu, token tiles).  A clip's items (tile_count)
 // are n_frames x n_strips for the fast variants, 0 for generic.  Integer / f64 exact.
 // ------------------------------------------------------------------------------------------
-enum { KV_MILD = 0, KV_MEDIUM = 1, KV_STRONG = 2, KV_GENERIC = 3, KV_COPY = 4, KV_TEAM = 5, KV_WIDE = 6, KV_DIRECT = 7 };
+enum { KV_MILD = 0, KV_MEDIUM = 1, KV_STRONG = 2, KV_GENERIC = 3, KV_COPY = 4, KV_TEAM = 5, KV_WIDE = 6, KV_DIRECT = 7,
+       KV_TEAML = 8 };
 constexpr int kGenericMaxTaps = 140;  // window-table length of the generic kernel (vp_resize.cu): ~34x per axis
 constexpr int kRing = 5;          // vertical ring slots: max live output rows per source row for in/out > 0.8
 constexpr int kInHMax = 1088;     // source rows supported by the fast kernel's per-row weight table
@@ -112,7 +113,8 @@ __host__ __device__ __forceinline__ int copy_wchunks(int grid_w, int m) { return
 constexpr int kTeamNV = 4, kTeamNH = 4, kTeamPPL = 1;    // V warps, H warps, column pairs per H lane
 constexpr int kWideNV = 10, kWideNH = 6, kWidePPL = 2;
 constexpr int kTeamUL = 10;       // union taps of a column pair (registers)
-constexpr int kTabInH = 1088;     // per-clip vertical weight records (float4 per source row)
+constexpr int kTeamULL = 32;      // KV_TEAML: union taps of a column pair for large downscales (unswizzled rows)
+constexpr int kTabInH = 2176;     // per-clip vertical weight records (float4 per source row)
 constexpr int kTabOutH = 1088;    // per-clip window ends (int per output row, padded to a multiple of 4)
 
 struct TeamGeo {
@@ -170,12 +172,18 @@ __host__ __device__ __forceinline__ int select_variant(int in_h, int in_w, int o
   // live output rows per source row <= floor(4/s)+1 for upscale (<= 5 iff s > 0.8) and <= 5 for downscale
   // (trimmed windows; brute-forced in tests/test_oracle_pixels.py::test_live_rows_bound).  The streaming kernel
   // stores column pairs (bf16x2 / float2), so it needs an even patch size.
-  if ((p & 1) || !(sv > 0.8) || in_h > kInHMax || out_h > kOutHMax) return generic_or_direct(in_h, in_w, out_h, out_w);
   const double sh = (double)in_w / (double)out_w;
-  if (sh < 0.6 || fast_strip_width(in_w, out_w) < 16) return generic_or_direct(in_h, in_w, out_h, out_w);
-  const int th = axis_max_taps(in_w, out_w);
-  for (int v = KV_MILD; v <= KV_STRONG; ++v)
-    if (th <= fast_lhm(v)) return v;
+  if (!(p & 1) && sv > 0.8 && in_h <= kInHMax && out_h <= kOutHMax && sh >= 0.6 && fast_strip_width(in_w, out_w) >= 16) {
+    const int th = axis_max_taps(in_w, out_w);
+    for (int v = KV_MILD; v <= KV_STRONG; ++v)
+      if (th <= fast_lhm(v)) return v;
+  }
+  // KV_TEAML (clips the fast streaming kernel cannot take, e.g. 1440p-4K sources at the Qwen budgets): the KV_TEAM
+  // structure with column-pair windows up to kTeamULL taps; the 4-slot vertical ring holds for every downscale
+  // (<= 4 live rows per source row)
+  if (in_h >= out_h && in_w >= out_w && (p & 1) == 0 && in_h <= kTabInH && out_h <= kTabOutH &&
+      pair_union_bound(in_w, out_w) <= kTeamULL && team_geometry(in_w, out_w, p, kTeamNV, variant_nh(KV_TEAM)).ws > 0)
+    return KV_TEAML;
   return generic_or_direct(in_h, in_w, out_h, out_w);
 }
 

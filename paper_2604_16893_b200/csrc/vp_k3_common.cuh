@@ -175,8 +175,8 @@ __device__ __forceinline__ int vfind(const VIdx& vx, int cnt, int64_t item) {   
   return lo;
 }
 
-// Per-variant work-index slots (variant_index_kernel): MILD, MEDIUM, STRONG, COPY, TEAM, WIDE.
-constexpr int kNSlots = 6;
+// Per-variant work-index slots (variant_index_kernel): MILD, MEDIUM, STRONG, COPY, TEAM, WIDE, TEAML.
+constexpr int kNSlots = 7;
 
 // Caller workspace of vp_resize_normalize_patchify (resize_ws_layout): the per-variant work index and the
 // KV_TEAM per-clip tables.  Nothing persists between calls.

@@ -149,7 +149,7 @@ plan_kernel(vp_params P, const vp_clip_desc* __restrict__ clips, int n, vp_clip_
       atomicOr(&s_variants, 1 << kv);
       if (kv == KV_COPY) {
         v[S_TILES] = (int64_t)r.n * (r.gh / P.merge_size) * copy_wchunks(r.gw, P.merge_size);
-      } else if (kv == KV_TEAM || kv == KV_WIDE) {
+      } else if (kv == KV_TEAM || kv == KV_WIDE || kv == KV_TEAML) {
         v[S_TILES] = (int64_t)r.n *
                      team_geometry(clips[k].width, r.out_w, P.patch_size, variant_nv(kv), variant_nh(kv)).nslices;
       } else if (kv != KV_GENERIC) {

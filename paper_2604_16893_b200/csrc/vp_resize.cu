@@ -414,11 +414,11 @@ extern "C" vp_status vp_resize_normalize_patchify(const vp_params* p, const vp_c
   auto has = [&](int kv) { return (mask >> kv) & 1u; };
   const int fast_aligned = (reinterpret_cast<uintptr_t>(frames) & 15) == 0;
   const bool any_fast = has(vp::KV_MILD) || has(vp::KV_MEDIUM) || has(vp::KV_STRONG) || has(vp::KV_COPY) ||
-                        has(vp::KV_TEAM) || has(vp::KV_WIDE);
+                        has(vp::KV_TEAM) || has(vp::KV_WIDE) || has(vp::KV_TEAML);
   if (fast_aligned && any_fast) {
     const vp::FKParams fk = vp::make_fkparams(p);
     cudaError_t e = vp::launch_index(plans, n, clip_byte_offset, row_pitch, ws, s);
-    if (e == cudaSuccess && (has(vp::KV_TEAM) || has(vp::KV_WIDE)))
+    if (e == cudaSuccess && (has(vp::KV_TEAM) || has(vp::KV_WIDE) || has(vp::KV_TEAML)))
       e = vp::launch_team(fk, plans, n, ws, frames, clip_byte_offset, row_pitch, pixel_values_images, img_rows_cap,
                           pixel_values_videos, vid_rows_cap, clip_status, dev, sms, mask, s);
     if (e == cudaSuccess)

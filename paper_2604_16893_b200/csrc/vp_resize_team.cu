@@ -52,15 +52,18 @@ constexpr int kNR = VP_TEAM_NR;             // retire slots (rows V may run ahea
 #define VP_ALL_LANES_ARRIVE 0
 #endif
 
-template <int NV, int NH>
+template <int NV, int NH, bool kLarge = false>
 struct SplitCfg {
   static constexpr int kPx = NV * 128;                                    // footprint pixels per CTA
+  // retire-slot stride in pixels: KV_TEAML keeps rows unswizzled with kTeamULL zero pixels of tail padding, so every
+  // tap of a pair window is base + 16 u (no per-tap address registers, no clamping)
+  static constexpr int kPxPad = kLarge ? kPx + kTeamULL : kPx;
   static constexpr int kThreads = (NV + NH) * 32;
   static constexpr int kRowB = (NV * 384 + 16 + 15) & ~15;                // staged row: footprint + alignment slack
   static constexpr size_t OFF_STG = 0;
   static constexpr size_t OFF_WREC = OFF_STG + (size_t)kTDepth * kRowB;
   static constexpr size_t OFF_BUF = OFF_WREC + (size_t)kTDepth * 16;
-  static constexpr size_t OFF_SBAR = OFF_BUF + (size_t)kNR * kPx * 16;
+  static constexpr size_t OFF_SBAR = OFF_BUF + (size_t)kNR * kPxPad * 16;
   static constexpr size_t OFF_RBAR = OFF_SBAR + (size_t)kTNGrp * 8;
   static constexpr size_t OFF_CNT = OFF_RBAR + (size_t)2 * kNR * 8;
   static constexpr size_t OFF_PROD = (OFF_CNT + (size_t)kTNGrp * 4 + 15) & ~(size_t)15;
@@ -184,15 +187,17 @@ __device__ __forceinline__ void store_pair(const FKParams& kp, char* q, float2 a
   }
 }
 
-template <int NV, int NH, int PPL, int kUL, bool kF32, bool kFold, int P, int M, int TP, int MINB>
+template <int NV, int NH, int PPL, int kUL, bool kF32, bool kFold, int P, int M, int TP, int MINB, bool kLarge>
 __global__ void __launch_bounds__((NV + NH) * 32, MINB)
 resize_split_kernel(FKParams kp, const vp_clip_plan* __restrict__ plans, const VIdx vx, const int* __restrict__ tab_alias,
                     const int* __restrict__ tab_flag, const float4* __restrict__ vtab, const int* __restrict__ y1tab,
                     const uint8_t* __restrict__ frames, const int64_t* __restrict__ clip_off,
                     const int64_t* __restrict__ pitch_arr, void* pv_img, int64_t img_cap, void* pv_vid, int64_t vid_cap,
                     int32_t* __restrict__ clip_status) {
-  using Cfg = SplitCfg<NV, NH>;
+  using Cfg = SplitCfg<NV, NH, kLarge>;
   constexpr int kPx = Cfg::kPx;
+  static_assert(!kLarge || (PPL == 1 && kUL <= kTeamULL), "KV_TEAML: one pair per lane, padded rows");
+  auto pos = [](int x) { return kLarge ? x : tpos(x); };     // retired-row pixel position
   constexpr int kRowB = Cfg::kRowB;
   // preset geometry (p % 4 == 0 and p*m % 4 == 0): every out_h is a multiple of 4, so with 4 retire slots the slot of
   // output row i is i % 4 = the static unroll index U
@@ -221,7 +226,7 @@ resize_split_kernel(FKParams kp, const vp_clip_plan* __restrict__ plans, const V
   TeamProd* ps = reinterpret_cast<TeamProd*>(smem + Cfg::OFF_PROD);
   float4* buf0 = reinterpret_cast<float4*>(smem + Cfg::OFF_BUF);
   const uint32_t buf_s = smem_u32(buf0);
-  constexpr uint32_t kSlotB = (uint32_t)kPx * 16;     // bytes per retire slot
+  constexpr uint32_t kSlotB = (uint32_t)Cfg::kPxPad * 16;   // bytes per retire slot
 
   // ---- staging producer: refill group g with the next kTGrp source rows of the CTA's item sequence (warp-uniform
   //      caller; the copies and barrier operations are predicated to lane 0) ----
@@ -282,7 +287,7 @@ resize_split_kernel(FKParams kp, const vp_clip_plan* __restrict__ plans, const V
     z.src = nullptr; z.wr = nullptr; z.pitch = 0; z.next = my_a; z.rows = 0; z.nbytes = 0;
     *ps = z;
   }
-  for (int i = tid; i < kNR * kPx; i += Cfg::kThreads) buf0[i] = make_float4(0.f, 0.f, 0.f, 0.f);
+  for (int i = tid; i < kNR * Cfg::kPxPad; i += Cfg::kThreads) buf0[i] = make_float4(0.f, 0.f, 0.f, 0.f);
   __syncthreads();
   if (warp == 0)
     for (uint32_t g = 0; g < kTNGrp; ++g) issue_group(g);   // prefill
@@ -291,7 +296,8 @@ resize_split_kernel(FKParams kp, const vp_clip_plan* __restrict__ plans, const V
     // ================================================================= V warps
     const uint32_t stage_s = smem_u32(stage), wrec_s = smem_u32(wrec);
     // retire address of this lane's 4 pixels (pixel 128*warp + 4*lane + k at +128k) in retire slot 0
-    const uint32_t vsa = buf_s + (uint32_t)tpos(warp * 128 + lane * 4) * 16u;
+    const uint32_t vsa = buf_s + (uint32_t)pos(warp * 128 + lane * 4) * 16u;
+    constexpr uint32_t kPxB = kLarge ? 16u : 128u;  // distance of the lane's consecutive pixels in the retired row
     uint32_t rc = 0;                              // staged rows consumed: slot rc % kTDepth
     uint32_t rr = 0;                              // output rows retired (all items)
     for (int64_t item = my_a; item < my_b; ++item) {
@@ -343,9 +349,9 @@ resize_split_kernel(FKParams kp, const vp_clip_plan* __restrict__ plans, const V
         const uint32_t ra = vsa + rs * kSlotB;                                                                \
         const float4* a = acc[U];                     /* pixels 0..2 are quads .xyz; pixel 3 is the .w column */ \
         sts_f4(ra, a[0]);                                                                                     \
-        sts_f4(ra + 128, a[1]);                                                                               \
-        sts_f4(ra + 256, a[2]);                                                                               \
-        sts_f4(ra + 384, make_float4(a[0].w, a[1].w, a[2].w, 0.f));                                           \
+        sts_f4(ra + kPxB, a[1]);                                                                              \
+        sts_f4(ra + 2 * kPxB, a[2]);                                                                          \
+        sts_f4(ra + 3 * kPxB, make_float4(a[0].w, a[1].w, a[2].w, 0.f));                                      \
         _Pragma("unroll") for (int q = 0; q < 3; ++q) acc[U][q] = make_float4(0.f, 0.f, 0.f, 0.f);            \
         __syncwarp();                                                                                         \
         mbar_arrive_if(&rfull[rs], l0 || VP_ALL_LANES_ARRIVE);                                                \
@@ -422,7 +428,8 @@ resize_split_kernel(FKParams kp, const vp_clip_plan* __restrict__ plans, const V
           const float wa = (x >= w0.x0 && x < w0.x1) ? (float)(keys_d(((double)x - w0.c + 0.5) * w0.inv) / r0) : 0.f;
           const float wb = (x >= w1.x0 && x < w1.x1) ? (float)(keys_d(((double)x - w1.c + 0.5) * w1.inv) / r1) : 0.f;
           wp[pp][u] = kFold ? make_float2(wa * kp.scale[0], wb * kp.scale[0]) : make_float2(wa, wb);
-          toff[pp][u] = buf_s + (uint32_t)tpos(min(x - pa, kPx - 1)) * 16u;   // slack taps (weight 0) stay in the row
+          toff[pp][u] = kLarge ? buf_s + (uint32_t)(xu - pa + u) * 16u        // padded row: base + 16 u
+                               : buf_s + (uint32_t)tpos(min(x - pa, kPx - 1)) * 16u;   // slack taps (weight 0) stay in the row
         }
         const int jl0 = ja % B, wbk = ja / B, mw = jl0 / p, px = jl0 - mw * p;
         colpart[pp] = (wbk * m * m + mw) * D + px;
@@ -517,7 +524,8 @@ __device__ __forceinline__ double win_sum(const Win& w) {
 }
 
 __device__ __forceinline__ bool teamish(const vp_clip_plan& pl, int64_t coff, int64_t pitch) {
-  return pl.status == VP_OK && pl.tile_count > 0 && (pl.kernel_variant == KV_TEAM || pl.kernel_variant == KV_WIDE) &&
+  return pl.status == VP_OK && pl.tile_count > 0 &&
+         (pl.kernel_variant == KV_TEAM || pl.kernel_variant == KV_WIDE || pl.kernel_variant == KV_TEAML) &&
          ((coff | pitch) & 15) == 0;
 }
 
@@ -558,7 +566,7 @@ team_vtab_kernel(const vp_clip_plan* __restrict__ plans, const int64_t* __restri
 // belongs to: the clips of a run share one vertical table.
 constexpr int kIdxThreads = 1024;
 __device__ __forceinline__ int variant_slot(int kv) {
-  return kv == KV_COPY ? 3 : (kv == KV_TEAM ? 4 : (kv == KV_WIDE ? 5 : (kv <= KV_STRONG ? kv : -1)));
+  return kv == KV_COPY ? 3 : (kv == KV_TEAM ? 4 : (kv == KV_WIDE ? 5 : (kv == KV_TEAML ? 6 : (kv <= KV_STRONG ? kv : -1))));
 }
 
 __global__ void __launch_bounds__(kIdxThreads)
@@ -727,17 +735,17 @@ cudaError_t launch_index(const vp_clip_plan* plans, int n, const int64_t* coff, 
   return cudaGetLastError();
 }
 
-template <int NV, int NH, int PPL, int MINB, bool kF32>
+template <int NV, int NH, int PPL, int MINB, bool kF32, int kUL = kTeamUL, bool kLarge = false>
 void launch_split(const FKParams& kp, bool preset, const vp_clip_plan* plans, const VIdx& vx, const ResizeWs& w,
                   const uint8_t* frames, const int64_t* coff, const int64_t* pitch, void* pi, int64_t icap, void* pvv,
                   int64_t vcap, int32_t* clip_status, int dev, int num_sms, cudaStream_t s) {
-  using Cfg = SplitCfg<NV, NH>;
+  using Cfg = SplitCfg<NV, NH, kLarge>;
   // Qwen2.5/3-VL geometry (p16 m2 tp2) with compile-time output addressing, else runtime parameters
   // a channel-uniform scale (e.g. Qwen mean = std = 0.5) folds into the horizontal weights (store_pair)
   const bool fold = kp.scale[0] == kp.scale[1] && kp.scale[1] == kp.scale[2];
-  auto kern = preset ? (fold ? resize_split_kernel<NV, NH, PPL, kTeamUL, kF32, true, 16, 2, 2, MINB>
-                             : resize_split_kernel<NV, NH, PPL, kTeamUL, kF32, false, 16, 2, 2, MINB>)
-                     : resize_split_kernel<NV, NH, PPL, kTeamUL, kF32, false, 0, 0, 0, MINB>;
+  auto kern = preset ? (fold ? resize_split_kernel<NV, NH, PPL, kUL, kF32, true, 16, 2, 2, MINB, kLarge>
+                             : resize_split_kernel<NV, NH, PPL, kUL, kF32, false, 16, 2, 2, MINB, kLarge>)
+                     : resize_split_kernel<NV, NH, PPL, kUL, kF32, false, 0, 0, 0, MINB, kLarge>;
   set_smem_attr(kern, dev, (int)Cfg::SMEM);
   int per_sm = 0;
   cudaOccupancyMaxActiveBlocksPerMultiprocessor(&per_sm, kern, Cfg::kThreads, Cfg::SMEM);
@@ -752,7 +760,15 @@ cudaError_t launch_team(const FKParams& kp, const vp_clip_plan* plans, int n, co
   dim3 tg((kTabInH + 127) / 128, n);
   team_vtab_kernel<<<tg, 128, 0, s>>>(plans, coff, pitch, w.alias, w.vtab, w.y1tab, w.tflag);
   const bool preset = kp.p == 16 && kp.m == 2 && kp.tp == 2;
-  const bool team = (mask >> KV_TEAM) & 1u, wide = (mask >> KV_WIDE) & 1u;
+  const bool team = (mask >> KV_TEAM) & 1u, wide = (mask >> KV_WIDE) & 1u, large = (mask >> KV_TEAML) & 1u;
+  if (large) {
+    if (kp.out_f32)
+      launch_split<kTeamNV, kTeamNH, 1, 2, true, kTeamULL, true>(kp, preset, plans, ws_vidx(w, n, 6), w, frames, coff,
+                                                                pitch, pi, icap, pvv, vcap, clip_status, dev, num_sms, s);
+    else
+      launch_split<kTeamNV, kTeamNH, 1, 2, false, kTeamULL, true>(kp, preset, plans, ws_vidx(w, n, 6), w, frames, coff,
+                                                                 pitch, pi, icap, pvv, vcap, clip_status, dev, num_sms, s);
+  }
   if (kp.out_f32) {
     if (team)
       launch_split<kTeamNV, kTeamNH, kTeamPPL, 2, true>(kp, preset, plans, ws_vidx(w, n, 4), w, frames, coff, pitch, pi,

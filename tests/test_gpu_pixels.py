@@ -370,3 +370,23 @@ def test_synth_frames_match_host_generator():
         vp.synth_frames(kid, 12345, torch.tensor(ids, device="cuda"), H, W, out, row_pitch=pitch)
         got = out.cpu().numpy().reshape(len(ids), H, pitch)[:, :, : 3 * W].reshape(len(ids), H, W, 3)
         assert np.array_equal(got, I.frames_u8(kind, 12345, ids, H, W))
+
+
+KV_TEAML = 8
+
+
+@pytest.mark.parametrize("dtype", [0, 1])
+def test_team_large_downscales(dtype):
+    """KV_TEAML (the team kernel with unswizzled, padded retire rows and <= 32-tap column-pair windows): 1440p and
+    2160p sources at the cfg2 video budget (3.75x / 5.6x), 1200 source rows at a small budget, an odd frame count, next to a
+    cfg2-ratio clip (KV_WIDE) in the same call; every element vs the oracle."""
+    import paper_2604_16893_b200 as vp
+    pre = vp.VisualPreprocessor(max_frames=3, video_max_pixels=262144, out_dtype=dtype, mean=CLIP_MEAN, std=CLIP_STD)
+    clips = [I.clip(3, 1.0, 1440, 2560), I.clip(1, 1.0, 2160, 3840), I.clip(3, 1.0, 720, 1280)]
+    pl = _aligned_compare(pre, clips)
+    kv = pl.plans_host["kernel_variant"][: len(clips)].tolist()
+    assert kv[0] == KV_TEAML and kv[1] == KV_TEAML and kv[2] == KV_WIDE, kv
+    pre2 = vp.VisualPreprocessor(max_frames=2, video_max_pixels=65536, out_dtype=dtype)
+    pl2 = _aligned_compare(pre2, [I.clip(2, 1.0, 1200, 1920), I.clip(2, 1.0, 1080, 1920)])
+    kv2 = pl2.plans_host["kernel_variant"][:2].tolist()
+    assert kv2[0] == KV_TEAML and kv2[1] in (0, 1, 2), kv2      # <= 1088 source rows: the fast streaming kernel

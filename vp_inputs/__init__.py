@@ -98,6 +98,11 @@ def config(name: str):
         return qwen3_params(max_frames=64), [image(1024, 1024)] * 16 + [clip(1800, 30.0, 720, 1280)] * 8
     if name == "cfg5":   # GRPO rollout batch: 512 cfg2 clips
         return qwen3_params(max_frames=64), [clip(1800, 30.0, 720, 1280)] * 512
+    # other source resolutions at the cfg2 video budget, 16 clips of 60 s @ 30 fps each (bench side lines)
+    res = {"res480p": (480, 854), "res1080p": (1080, 1920), "res1440p": (1440, 2560), "res2160p": (2160, 3840)}
+    if name in res:
+        h, w = res[name]
+        return qwen3_params(max_frames=64), [clip(1800, 30.0, h, w)] * 16
     raise KeyError(name)
 
 
