@@ -27,37 +27,10 @@
 #include "vp_k3_common.cuh"
 #include <atomic>
 
-#ifndef VP_PLANAR
-// V->H rows as R / G / B planes (retire_planar): V saves its repacking moves (2.4% with H's taps off) but H's
-// 3 LDS.32 per tap and row cost more than that (4% slower overall on cfg5), so pixel-major is the default
-#define VP_PLANAR 0
-#endif
-#ifndef VP_CVT_I2F
-#define VP_CVT_I2F 2        // how many of the 3 staged words per row convert on XU (I2F) instead of PRMT+FADD2
-#endif
-#ifndef VP_H_SLEEP
-#define VP_H_SLEEP 0        // H warps wait for V rows with a suspend-time hint instead of spinning
-#endif
-#ifndef VP_VREGS
-#define VP_VREGS 152        // setmaxnreg split between the V and H warpgroups (sum 256)
-#endif
-#ifndef VP_HREGS
-#define VP_HREGS 104
-#endif
+// setmaxnreg split between the V and H warpgroups (sum 256): V needs its 152 registers
+constexpr int kVRegs = 152, kHRegs = 104;
 #ifndef VP_ALL_LANES_ARRIVE
 #define VP_ALL_LANES_ARRIVE 0   // verification build only (scripts/sanitize.sh): every lane arrives on vfull/vempty
-#endif
-#ifndef VP_EXP_NO_VMATH
-#define VP_EXP_NO_VMATH 0   // experiments only: skip the V ring FMAs
-#endif
-#ifndef VP_EXP_NO_HMATH
-#define VP_EXP_NO_HMATH 0   // experiments only: skip the H taps, normalisation and stores
-#endif
-#ifndef VP_EXP_NO_VWAIT
-#define VP_EXP_NO_VWAIT 0   // experiments only (scripts/exp3.sh): V does not wait for H to free rows
-#endif
-#ifndef VP_EXP_NO_HWAIT
-#define VP_EXP_NO_HWAIT 0   // experiments only: H does not wait for V rows (reads stale rows)
 #endif
 
 namespace vp {
@@ -140,9 +113,9 @@ __device__ __forceinline__ int vpos(int x) {
   x &= kRowPx - 1;                  // union-slack taps past the footprint (zero weight) wrap to finite data
   return (x & ~31) | ((x & 3) << 3) | ((x & 31) >> 2);
 }
-// byte offset of footprint pixel x inside a retired row (pixel-major float4 at vpos(x), or planar float at x)
+// byte offset of footprint pixel x inside a retired row (pixel-major float4 at vpos(x))
 __device__ __forceinline__ int hoff(int x) {
-  return VP_PLANAR ? (x & (kRowPx - 1)) * (int)sizeof(float) : vpos(x) * (int)sizeof(float4);
+  return vpos(x) * (int)sizeof(float4);
 }
 
 // store the finished output row of slot S as 4 pixel-major float4 (R, G, B, pad) at this lane's pixel
@@ -175,37 +148,6 @@ __device__ __forceinline__ void bytes_to_f2(uint32_t w, float2& lo, float2& hi) 
                               __uint_as_float(__byte_perm(w, 0x4B000000u, 0x7543u))), mm);
 }
 
-// Planar variant of the ring: the FFMA2 pairs are (R0,R1) (R2,R3) | (G0,G1) (G2,G3) | (B0,B1) (B2,B3), so each
-// accumulator quad holds one channel of the lane's 4 pixels and retires as one 16-B store into that channel's
-// plane (no repacking moves).  Staged words: n0 = R0 G0 B0 R1, n1 = G1 B1 R2 G2, n2 = B2 R3 G3 B3.
-__device__ __forceinline__ float byte_f_i2f(uint32_t w, int k) { return (float)((w >> (8 * k)) & 0xffu); }
-__device__ __forceinline__ float byte_f_magic(uint32_t w, int k) {      // 2^23 + b (subtract 2^23 after)
-  return __uint_as_float(__byte_perm(w, 0x4B000000u, 0x7540u + (unsigned)k));
-}
-__device__ __forceinline__ void bytes_to_planar(uint32_t n0, uint32_t n1, uint32_t n2, float2 (&f)[6]) {
-  f[0] = make_float2(byte_f_i2f(n0, 0), byte_f_i2f(n0, 3));   // R0 R1
-  f[1] = make_float2(byte_f_i2f(n1, 2), byte_f_i2f(n2, 1));   // R2 R3
-  f[2] = make_float2(byte_f_i2f(n0, 1), byte_f_i2f(n1, 0));   // G0 G1
-  f[3] = make_float2(byte_f_i2f(n1, 3), byte_f_i2f(n2, 2));   // G2 G3
-  // 8 bytes on the XU pipe (I2F.U8), 4 on ALU + FMA (PRMT + FADD2), as in the pixel-major ring
-  const float2 mm = make_float2(-8388608.f, -8388608.f);
-  f[4] = __fadd2_rn(make_float2(byte_f_magic(n0, 2), byte_f_magic(n1, 1)), mm);   // B0 B1
-  f[5] = __fadd2_rn(make_float2(byte_f_magic(n2, 0), byte_f_magic(n2, 3)), mm);   // B2 B3
-}
-// Planar retired row: R plane at row[0, kRowPx), G at [kRowPx, 2 kRowPx), B at [2 kRowPx, 3 kRowPx) (floats,
-// natural pixel order).  V stores: lane L writes 16 B at pixel 4L of each plane (conflict-free); H tap reads:
-// 3 LDS.32 per tap and row at 1.75 wavefronts each at the cfg2 ratio (offline bank simulation), i.e. about
-// the smem traffic of the pixel-major LDS.128 (1.35 x 4).
-template <int S>
-__device__ __forceinline__ void retire_planar(Acc& acc, float* __restrict__ row, int px, bool active) {
-  if (active) {
-    *reinterpret_cast<float4*>(row + px) = acc[S].q[0];
-    *reinterpret_cast<float4*>(row + kRowPx + px) = acc[S].q[1];
-    *reinterpret_cast<float4*>(row + 2 * kRowPx + px) = acc[S].q[2];
-  }
-#pragma unroll
-  for (int j = 0; j < 3; ++j) acc[S].q[j] = make_float4(0.f, 0.f, 0.f, 0.f);
-}
 
 template <bool kF32>
 __device__ __forceinline__ void store_slots(void* pv, int64_t idx, float v0, float v1, int nslots, int ti0, int tp,
@@ -343,7 +285,7 @@ resize_fast_kernel(FKParams kp, const vp_clip_plan* __restrict__ plans, const VI
 
   if (warp < kNVW) {
     // ============================================================ V warps: vertical ring
-    asm volatile("setmaxnreg.inc.sync.aligned.u32 %0;\n" :: "n"(VP_VREGS) : "memory");
+    asm volatile("setmaxnreg.inc.sync.aligned.u32 %0;\n" :: "n"(kVRegs) : "memory");
     uint8_t* stage = stage_all + (size_t)warp * kDepth * kWarpB;
     uint64_t* full = full_all + warp * kNGrp;     // one barrier per group of kGrp staging slots
     uint64_t* ebar = ebar_all + warp * kNGrp;     // verification build: the warp's reads of a group are done
@@ -479,13 +421,9 @@ resize_fast_kernel(FKParams kp, const vp_clip_plan* __restrict__ plans, const VI
               const float4 wa = w4t[y];                                                         \
               const float wb = w1t[y];                                                          \
               float2 fv[6];                   /* bytes (2q, 2q+1) as exact floats (PRMT + FADD2) */ \
-              if (VP_PLANAR) {                                                                  \
-                bytes_to_planar(n0, n1, n2, fv);                                                \
-              } else {                                                                          \
-              if (VP_CVT_I2F >= 1) bytes_to_f2_i2f(n0, fv[0], fv[1]); else bytes_to_f2(n0, fv[0], fv[1]); \
-              if (VP_CVT_I2F >= 2) bytes_to_f2_i2f(n1, fv[2], fv[3]); else bytes_to_f2(n1, fv[2], fv[3]); \
-              if (VP_CVT_I2F >= 3) bytes_to_f2_i2f(n2, fv[4], fv[5]); else bytes_to_f2(n2, fv[4], fv[5]); \
-              }                                                                                 \
+              bytes_to_f2_i2f(n0, fv[0], fv[1]);   /* 2 of 3 words on the XU pipe (I2F.U8) */   \
+              bytes_to_f2_i2f(n1, fv[2], fv[3]);                                                \
+              bytes_to_f2(n2, fv[4], fv[5]);       /* 1 on ALU + FMA (PRMT + FADD2) */          \
               const uint32_t used = rc++ % kDepth;                                              \
               if ((used & (kGrp - 1)) == kGrp - 1) {   /* group read: refill it */                \
                 __syncwarp();                                                                   \
@@ -493,12 +431,11 @@ resize_fast_kernel(FKParams kp, const vp_clip_plan* __restrict__ plans, const VI
                 issue_group(used / kGrp);                                                       \
               }                                                                                 \
               const float w5[kRing] = {wa.x, wa.y, wa.z, wa.w, wb};                             \
-              if (!VP_EXP_NO_VMATH) ring_row<U>(acc, w5, fv);                                   \
+              ring_row<U>(acc, w5, fv);                                                         \
             }                                                                                   \
             const uint32_t vs = vslot, vp2 = vs >> 1, vph = vphase;                             \
-            if ((vs & 1) == 0 && !VP_EXP_NO_VWAIT) mbar_wait(&vempty[vp2], vph ^ 1);    /* per pair */ \
-            if (VP_PLANAR) retire_planar<U>(acc, reinterpret_cast<float*>(vbuf + vs * kRowPx), px_lane, vactive); \
-            else retire_slot<U>(acc, vbuf + vs * kRowPx, vb, vactive);                          \
+            if ((vs & 1) == 0) mbar_wait(&vempty[vp2], vph ^ 1);    /* per pair */              \
+            retire_slot<U>(acc, vbuf + vs * kRowPx, vb, vactive);                               \
             __syncwarp();                                                                       \
             if (lane == 0 || VP_ALL_LANES_ARRIVE) mbar_arrive(&vfull[vp2]);                                            \
             if (++vslot == kCapR) { vslot = 0; vphase ^= 1; }                                   \
@@ -530,7 +467,7 @@ resize_fast_kernel(FKParams kp, const vp_clip_plan* __restrict__ plans, const VI
   }
 
   // ============================================================ H warps: horizontal pass + store
-  asm volatile("setmaxnreg.dec.sync.aligned.u32 %0;\n" :: "n"(VP_HREGS) : "memory");
+  asm volatile("setmaxnreg.dec.sync.aligned.u32 %0;\n" :: "n"(kHRegs) : "memory");
   const int ht = tid - kNVW * 32;       // 0..127
   const int p = kp.p, m = kp.m, tp = kp.tp, B = m * p;
   uint32_t vrow = 0;
@@ -611,15 +548,12 @@ resize_fast_kernel(FKParams kp, const vp_clip_plan* __restrict__ plans, const VI
       for (int i = 0; i < out_h; i += 2) {
         const bool two = i + 1 < out_h;
         const uint32_t s0 = vrow % kCapR, s1 = s0 + 1, ph0 = (vrow / kCapR) & 1;   // rows of pair s0/2
-        if (!VP_EXP_NO_HWAIT) {
-          if (VP_H_SLEEP) mbar_wait_sleep(&vfull[s0 >> 1], ph0);
-          else mbar_wait(&vfull[s0 >> 1], ph0);
-        }
+        mbar_wait(&vfull[s0 >> 1], ph0);
         const int64_t rp0 = rbase + rp;
         advance_row();
         const int64_t rp1 = rbase + rp;
         if (two) advance_row();
-        if (writable && hact && !VP_EXP_NO_HMATH) {
+        if (writable && hact) {
           // row bases (warp-uniform) + per-lane byte offsets: one LDS.128 [R + UR] per tap and row
           const char* v0 = reinterpret_cast<const char*>(vbuf + s0 * kRowPx);
           const char* v1 = reinterpret_cast<const char*>(vbuf + (two ? s1 : s0) * kRowPx);
@@ -631,16 +565,8 @@ resize_fast_kernel(FKParams kp, const vp_clip_plan* __restrict__ plans, const VI
           for (int u = 0; u < UL; ++u) {
             const float2 wp = wr[u];                           // (col a, col b) weights at pixel xu+u
             const int o = UL <= 11 ? toff[u < kOffRegs ? u : 0] : hoff(xu + u);
-            float4 q0, q1;                                     // rows i, i+1 (.xyz = R, G, B)
-            if (VP_PLANAR) {
-              const float* p0 = reinterpret_cast<const float*>(v0 + o);
-              const float* p1 = reinterpret_cast<const float*>(v1 + o);
-              q0 = make_float4(p0[0], p0[kRowPx], p0[2 * kRowPx], 0.f);
-              q1 = make_float4(p1[0], p1[kRowPx], p1[2 * kRowPx], 0.f);
-            } else {
-              q0 = *reinterpret_cast<const float4*>(v0 + o);
-              q1 = *reinterpret_cast<const float4*>(v1 + o);
-            }
+            const float4 q0 = *reinterpret_cast<const float4*>(v0 + o);   // rows i, i+1 (.xyz = R, G, B)
+            const float4 q1 = *reinterpret_cast<const float4*>(v1 + o);
             ar0 = __ffma2_rn(make_float2(q0.x, q0.x), wp, ar0);
             ag0 = __ffma2_rn(make_float2(q0.y, q0.y), wp, ag0);
             ab0 = __ffma2_rn(make_float2(q0.z, q0.z), wp, ab0);

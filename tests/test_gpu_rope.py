@@ -163,3 +163,39 @@ def test_presets_end_to_end(name):
     ids, od, ost, bst = O.rope_index(seqs, ig, vg, m, variant=pre.rope_variant, second_per_grid_ts=ref_spg,
                                      tokens_per_second=pre.tokens_per_second)
     assert np.array_equal(pos.cpu().numpy(), np.concatenate(ids, axis=1)) and deltas.cpu().tolist() == od
+
+
+def test_ac9_strict_alignment_fuzz_10000_batches():
+    """S:662 AC9 at its stated scale: 10,000 random batches (1-6 sequences of text / image / video runs) with
+    adversarial off-by-one runs, glued video groups and missing grids; statuses, ids and deltas vs the oracle.
+    Batches are concatenated 100 at a time into one packed call (sequence statuses are per sequence; the batch
+    status is checked per call)."""
+    rng = random.Random(9000)
+    m = 2
+    checked = 0
+    for call in range(100):
+        img, vid, seqs = [], [], []
+        for _ in range(100):                             # 100 batches of 1-6 sequences per packed call
+            for _ in range(rng.randint(1, 6)):
+                runs = [(0, rng.randint(0, 6))]
+                for _ in range(rng.randint(0, 3)):
+                    if rng.random() < 0.5:
+                        g = (1, 2 * rng.randint(1, 6), 2 * rng.randint(1, 6))
+                        img.append(g)
+                        n = g[1] * g[2] // 4 + (rng.choice([-1, 1]) if rng.random() < 0.15 else 0)
+                        runs += [(1, max(n, 1)), (0, rng.randint(1, 3))]
+                    else:
+                        g = (rng.randint(1, 3), 2 * rng.randint(1, 4), 2 * rng.randint(1, 4))
+                        vid.append(g)
+                        for gi in range(g[0]):
+                            n = g[1] * g[2] // 4 + (rng.choice([-1, 1]) if rng.random() < 0.08 else 0)
+                            runs += [(0, rng.randint(1, 3)) if (gi == 0 or rng.random() > 0.05) else (0, 0),
+                                     (2, max(n, 1))]
+                        runs.append((0, rng.randint(1, 2)))
+                runs = [r for r in runs if r[1] > 0]
+                seqs.append(I.token_types(runs))
+            checked += 1
+        if rng.random() < 0.2 and img:
+            img.pop()
+        _compare(seqs, img, vid, m)
+    assert checked == 10000
