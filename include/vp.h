@@ -55,12 +55,17 @@ typedef enum { VP_BUDGET_PER_FRAME = 0 /* P:271 */, VP_BUDGET_TOTAL = 1 /* Qwen3
 typedef enum { VP_ROPE_QWEN3_SPLIT = 0 /* C18 */, VP_ROPE_QWEN2 = 1 /* classic, C19 */,
                VP_ROPE_QWEN25 = 2 /* time-scaled, C19 */ } vp_rope_variant;
 typedef enum { VP_OUT_BF16 = 0, VP_OUT_F32 = 1 } vp_dtype;
+typedef enum { VP_RESIZE_FLOAT = 0 /* C11: float domain end to end, one clamp after the second pass */,
+               VP_RESIZE_U8 = 1    /* N1 HF drop-in: torch's uint8 antialiased bicubic, bit-exact -- int16-precision
+                                      coefficients (p = max bits with max|w|*2^p < 2^15), horizontal pass first,
+                                      u8 (clamped, >> p with 2^(p-1) rounding) between and after the passes;
+                                      downscales <= 15.5x per axis (else VP_EUNSUPPORTED) */ } vp_resize_mode;
 typedef enum { VP_SYNTH_RAMP = 0 /* S:71 */, VP_SYNTH_NOISE = 1 } vp_synth_kind;
 
 /* Preprocessing parameters (S:29-34 PreprocessParams; P:90 independent budgets; P:271 values).
  * Invariants checked on the host (VP_EINVAL): patch,merge,tp >= 1; max_frames >= tp;
  * video_max_pixels, image_max_pixels >= (patch*merge)^2; target_fps > 0; std[c] != 0; sampling in vp_sampling;
- * 0 <= min_frames <= max_frames. */
+ * 0 <= min_frames <= max_frames; resize_mode in vp_resize_mode. */
 typedef struct {
   double  target_fps;          /* 2.0 */
   int32_t max_frames;          /* 128 */
@@ -80,7 +85,7 @@ typedef struct {
                                   variants are not launched.  0 = unknown: launch every kernel.  Ignored by the
                                   other calls.  A mask missing a present variant leaves its clips unwritten. */
   int32_t min_frames;          /* VP_SAMPLE_LINSPACE only: lower clamp of n (HF Qwen3-VL: 4) */
-  int32_t reserved_;           /* 0 */
+  int32_t resize_mode;         /* vp_resize_mode (plan and resize calls must agree) */
 } vp_params;                   /* 120 bytes */
 
 /* One input clip (S:42-47 VideoMetadata source fields).  Images: is_image=1, the frame count and
@@ -179,7 +184,8 @@ vp_status vp_plan_frames(const vp_params* p, const vp_clip_desc* clips, int32_t 
  *   pixel_values_videos (dev, nullable if no videos) [vid_rows_cap, 3*tp*p*p] of out_dtype
  *   image_grid_thw, video_grid_thw (dev) [n_images,3] / [n_videos,3] int64 (HF convention)
  *   clip_status (dev, nullable) [n] int32 output: VP_OK, VP_EINVAL (invalid plan), VP_ECAPACITY
- *                      (rows beyond the cap; that clip's rows are not written).  Every resize ratio is
+ *                      (rows beyond the cap; that clip's rows are not written) or VP_EUNSUPPORTED (VP_RESIZE_U8
+ *                      beyond 15.5x; rows not written).  In VP_RESIZE_FLOAT mode every resize ratio is
  *                      supported (downscales beyond the shared-memory window tables, ~34x per axis, take a
  *                      direct f64 kernel)
  *   workspace (dev)    vp_resize_workspace_bytes(n) bytes, 256-B aligned, caller-owned scratch (work index and

@@ -31,7 +31,7 @@ __all__ = [
     "keys_cubic", "aa_weights", "weight_matrix", "resize_frame", "resize_pixel",
     "normalize", "temporal_pad", "patchify", "patch_coords", "bf16_rne_bits", "bf16_bits_to_f64",
     "group_timestamps", "hf_sampled_fps", "second_per_grid", "qwen25_interval", "rope_index", "process_batch", "ClipPlan",
-    "dedup_keys", "nv12_to_rgb", "vision_pos_ids", "vision_cu_seqlens",
+    "dedup_keys", "quantize_weights_u8", "resize_frame_u8", "nv12_to_rgb", "vision_pos_ids", "vision_cu_seqlens",
 ]
 
 VP_OK, VP_EINVAL, VP_EMISMATCH = 0, 1, 3
@@ -275,6 +275,61 @@ def aa_weights(in_size: int, out_size: int):
     return out
 
 
+def quantize_weights_u8(in_size: int, out_size: int):
+    """N1 (HF drop-in: HF resizes uint8 frames on torch's uint8 antialiased path, reading C11): the aa_weights of an
+    axis as int16 fixed-point coefficients.  Precision p = the largest p <= 22 with max|w| * 2^(p+1) >= 2^15 not yet
+    reached, i.e. max|w| * 2^p < 2^15; c = w * 2^p rounded half away from zero.  Returns ([(x0, [c...])], p)."""
+    # the C10 window and weights, normalised with a sequential sum (as the integer path sums them; a last-ulp
+    # difference could flip a coefficient's rounding)
+    scale = float(in_size) / float(out_size)
+    fs = max(scale, 1.0)
+    ws = []
+    for i in range(out_size):
+        c = (i + 0.5) * scale
+        x0 = max(0, int(c - 2.0 * fs + 0.5))
+        x1 = min(in_size, int(c + 2.0 * fs + 0.5))
+        w = [keys_cubic((k + x0 - c + 0.5) * (1.0 / fs)) for k in range(x1 - x0)]
+        tot = 0.0
+        for v in w:
+            tot += v
+        ws.append((x0, [v / tot for v in w] if tot != 0.0 else w))
+    mx = max(max(abs(v) for v in w) for _, w in ws)
+    p = 0
+    while p < 22 and mx * float(1 << (p + 1)) < float(1 << 15):
+        p += 1
+    q = []
+    for x0, w in ws:
+        q.append((x0, [int(v * (1 << p) + 0.5) if v >= 0 else int(v * (1 << p) - 0.5) for v in w]))
+    return q, p
+
+
+def resize_frame_u8(frame_u8: np.ndarray, out_h: int, out_w: int) -> np.ndarray:
+    """N1: separable AA bicubic in integers, horizontal pass first (when out_w != W), then vertical (when
+    out_h != H); each pass: acc = 2^(p-1) + sum_k c_k * x_k, out = clamp(acc >> p, 0, 255) as u8 (so the
+    intermediate is quantised, unlike O5).  frame_u8 [H, W, 3] -> u8 [out_h, out_w, 3]."""
+    x = frame_u8.astype(np.int64)
+    H, W, _ = x.shape
+    if out_w != W:
+        q, p = quantize_weights_u8(W, out_w)
+        y = np.zeros((H, out_w, 3), dtype=np.int64)
+        for j, (x0, c) in enumerate(q):
+            acc = np.full((H, 3), 1 << (p - 1), dtype=np.int64)
+            for k, ck in enumerate(c):
+                acc += ck * x[:, x0 + k, :]
+            y[:, j, :] = np.clip(acc >> p, 0, 255)
+        x = y
+    if out_h != H:
+        q, p = quantize_weights_u8(H, out_h)
+        y = np.zeros((out_h, x.shape[1], 3), dtype=np.int64)
+        for i, (y0, c) in enumerate(q):
+            acc = np.full((x.shape[1], 3), 1 << (p - 1), dtype=np.int64)
+            for k, ck in enumerate(c):
+                acc += ck * x[y0 + k, :, :]
+            y[i] = np.clip(acc >> p, 0, 255)
+        x = y
+    return x.astype(np.uint8)
+
+
 def weight_matrix(in_size: int, out_size: int) -> np.ndarray:
     """Dense [out, in] operator of aa_weights (zeros outside each window)."""
     M = np.zeros((out_size, in_size), dtype=np.float64)
@@ -499,7 +554,10 @@ def process_batch(params: dict, clips, frames_list, plans=None):
     for pl, fr in zip(plans, frames_list):
         if pl.status != VP_OK:
             continue
-        res = np.stack([resize_frame(fr[k], pl.out_h, pl.out_w) for k in range(pl.n)])
+        if params.get("resize_mode", 0) == 1:        # N1: u8-quantised resize (torch uint8 AA path)
+            res = np.stack([resize_frame_u8(fr[k], pl.out_h, pl.out_w) for k in range(pl.n)]).astype(np.float64)
+        else:
+            res = np.stack([resize_frame(fr[k], pl.out_h, pl.out_w) for k in range(pl.n)])
         xn = normalize(res, params["mean"], params["std"])
         rows = patchify(xn, p, m, tp)
         (img_rows if pl.is_image else vid_rows).append(rows)

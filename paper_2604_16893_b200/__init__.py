@@ -16,7 +16,8 @@ import torch
 from .presets import PRESETS, preset
 from ._lib import (DESC_DTYPE, PLAN_DTYPE, TOT, TOT_LEN, VP_BUDGET_PER_FRAME, VP_BUDGET_TOTAL, VP_ECAPACITY,
                    VP_EINVAL, VP_EMISMATCH, VP_EUNSUPPORTED, VP_OK, VP_OUT_BF16, VP_OUT_F32, VP_ROPE_QWEN2,
-                   VP_ROPE_QWEN3_SPLIT, VP_ROPE_QWEN25, VP_SAMPLE_CENTER_BIN, VP_SAMPLE_LINSPACE, VP_SYNTH_NOISE,
+                   VP_ROPE_QWEN3_SPLIT, VP_ROPE_QWEN25, VP_RESIZE_FLOAT, VP_RESIZE_U8, VP_SAMPLE_CENTER_BIN,
+                   VP_SAMPLE_LINSPACE, VP_SYNTH_NOISE,
                    VP_SYNTH_RAMP, VpError, VpParams,
                    check, lib)
 
@@ -28,7 +29,7 @@ __all__ = [
     "VisualPreprocessor",
     "PlacementMismatch", "VpError", "VpParams", "DESC_DTYPE", "PLAN_DTYPE", "TOT", "TOT_LEN",
     "VP_ROPE_QWEN3_SPLIT", "VP_ROPE_QWEN2", "VP_ROPE_QWEN25", "VP_OUT_BF16", "VP_OUT_F32",
-    "VP_SAMPLE_CENTER_BIN", "VP_SAMPLE_LINSPACE",
+    "VP_SAMPLE_CENTER_BIN", "VP_SAMPLE_LINSPACE", "VP_RESIZE_FLOAT", "VP_RESIZE_U8",
     "VP_BUDGET_PER_FRAME", "VP_BUDGET_TOTAL", "VP_SYNTH_RAMP", "VP_SYNTH_NOISE", "VP_OK", "VP_EINVAL",
     "VP_EMISMATCH", "VP_ECAPACITY", "VP_EUNSUPPORTED", "lib",
 ]
@@ -54,7 +55,7 @@ def _stream(stream) -> int | None:
 
 def make_params(target_fps=2.0, max_frames=128, temporal_patch_size=2, patch_size=16, merge_size=2,
                 video_max_pixels=262144, image_max_pixels=1048576, min_pixels=0, budget_mode=0, sampling=0,
-                mean=(0.5, 0.5, 0.5), std=(0.5, 0.5, 0.5), out_dtype=VP_OUT_BF16, min_frames=None) -> VpParams:
+                mean=(0.5, 0.5, 0.5), std=(0.5, 0.5, 0.5), out_dtype=VP_OUT_BF16, min_frames=None, resize_mode=0) -> VpParams:
     """vp_params (defaults = Qwen3-VL preset with the P:271 budgets)."""
     p = VpParams()
     p.target_fps, p.max_frames, p.temporal_patch_size = float(target_fps), int(max_frames), int(temporal_patch_size)
@@ -62,6 +63,7 @@ def make_params(target_fps=2.0, max_frames=128, temporal_patch_size=2, patch_siz
     p.video_max_pixels, p.image_max_pixels, p.min_pixels = int(video_max_pixels), int(image_max_pixels), int(min_pixels)
     p.budget_mode, p.sampling, p.out_dtype = int(budget_mode), int(sampling), int(out_dtype)
     p.min_frames = min(4, p.max_frames) if min_frames is None else int(min_frames)   # HF Qwen3-VL: 4
+    p.resize_mode = int(resize_mode)
     for c in range(3):
         p.mean[c], p.std[c] = float(mean[c]), float(std[c])
     return p

@@ -12,7 +12,7 @@ LIB = os.path.join(HERE, "libvp.so")
 ARCH = ["-gencode", "arch=compute_100a,code=sm_100a"]
 # vp_plan.cu carries the bit-exact f64 planning: no FMA contraction there (SURVEY §7 hard parts).
 PER_FILE = {"vp_plan.cu": ["--fmad=false"]}
-SOURCES = ["vp_abi.cu", "vp_adjacent.cu", "vp_dedup.cu", "vp_plan.cu", "vp_resize.cu", "vp_resize_fast.cu", "vp_resize_team.cu", "vp_rope.cu", "vp_synth.cu"]
+SOURCES = ["vp_abi.cu", "vp_adjacent.cu", "vp_dedup.cu", "vp_plan.cu", "vp_resize.cu", "vp_resize_fast.cu", "vp_resize_team.cu", "vp_resize_u8.cu", "vp_rope.cu", "vp_synth.cu"]
 
 
 def nvcc() -> str:

@@ -16,6 +16,7 @@ LIB_PATH = os.path.join(HERE, "libvp.so")
 VP_OK, VP_EINVAL, VP_EALIGN, VP_EMISMATCH, VP_ECAPACITY, VP_ECUDA, VP_EUNSUPPORTED = range(7)
 VP_ROPE_QWEN3_SPLIT, VP_ROPE_QWEN2, VP_ROPE_QWEN25 = 0, 1, 2
 VP_SAMPLE_CENTER_BIN, VP_SAMPLE_LINSPACE = 0, 1
+VP_RESIZE_FLOAT, VP_RESIZE_U8 = 0, 1
 VP_OUT_BF16, VP_OUT_F32 = 0, 1
 VP_BUDGET_PER_FRAME, VP_BUDGET_TOTAL = 0, 1
 VP_SYNTH_RAMP, VP_SYNTH_NOISE = 0, 1
@@ -37,7 +38,7 @@ class VpParams(C.Structure):
                 ("image_max_pixels", C.c_int64), ("min_pixels", C.c_int64), ("budget_mode", C.c_int32),
                 ("sampling", C.c_int32), ("mean", C.c_double * 3), ("std", C.c_double * 3),
                 ("out_dtype", C.c_int32), ("launch_mask", C.c_int32),
-                ("min_frames", C.c_int32), ("reserved_", C.c_int32)]
+                ("min_frames", C.c_int32), ("resize_mode", C.c_int32)]
 
 
 DESC_DTYPE = np.dtype([("total_source_frames", "<i8"), ("source_fps", "<f8"), ("height", "<i4"),

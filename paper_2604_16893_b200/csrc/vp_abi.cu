@@ -37,8 +37,9 @@ vp_status check_params(const vp_params* p) {
   }
   if (!(p->target_fps > 0.0) || p->min_pixels < 0 || (p->budget_mode != 0 && p->budget_mode != 1) ||
       (p->sampling != VP_SAMPLE_CENTER_BIN && p->sampling != VP_SAMPLE_LINSPACE) ||
-      (p->out_dtype != 0 && p->out_dtype != 1) || p->min_frames < 0 || p->min_frames > p->max_frames) {
-    set_error("params: invalid target_fps / min_pixels / budget_mode / sampling / out_dtype / min_frames");
+      (p->out_dtype != 0 && p->out_dtype != 1) || p->min_frames < 0 || p->min_frames > p->max_frames ||
+      (p->resize_mode != VP_RESIZE_FLOAT && p->resize_mode != VP_RESIZE_U8)) {
+    set_error("params: invalid target_fps / min_pixels / budget_mode / sampling / out_dtype / min_frames / resize_mode");
     return VP_EINVAL;
   }
   for (int c = 0; c < 3; ++c)

@@ -52,7 +52,9 @@ constexpr int kTotLen = VP_TOT_LEN;
 // are n_frames x n_strips for the fast variants, 0 for generic.  Integer / f64 exact.
 // ------------------------------------------------------------------------------------------
 enum { KV_MILD = 0, KV_MEDIUM = 1, KV_STRONG = 2, KV_GENERIC = 3, KV_COPY = 4, KV_TEAM = 5, KV_WIDE = 6, KV_DIRECT = 7,
-       KV_TEAML = 8 };
+       KV_TEAML = 8, KV_U8 = 9 };
+// KV_U8 (vp_resize_u8.cu, resize_mode = VP_RESIZE_U8): tiles of kU8Rows (fewer for s > 4) x kU8Cols output pixels
+constexpr int kU8Cols = 64, kU8Rows = 32, kU8MaxTaps = 64, kU8TileRows = 200;
 constexpr int kGenericMaxTaps = 140;  // window-table length of the generic kernel (vp_resize.cu): ~34x per axis
 constexpr int kRing = 5;          // vertical ring slots: max live output rows per source row for in/out > 0.8
 constexpr int kInHMax = 1088;     // source rows supported by the fast kernel's per-row weight table
@@ -160,7 +162,23 @@ __host__ __device__ __forceinline__ int generic_or_direct(int in_h, int in_w, in
   return 4.0 * fs + 2.0 > (double)kGenericMaxTaps ? KV_DIRECT : KV_GENERIC;
 }
 
-__host__ __device__ __forceinline__ int select_variant(int in_h, int in_w, int out_h, int out_w, int p) {
+__host__ __device__ __forceinline__ int u8_rows_per_band(int in_h, int out_h) {
+  const double s = (double)in_h / (double)out_h;
+  return max(1, kU8Rows / (int)ceil(fmax(s, 1.0) / 4.0));
+}
+__host__ __device__ __forceinline__ int64_t u8_tiles(int n_frames, int in_h, int out_h, int out_w) {
+  const int rb = u8_rows_per_band(in_h, out_h);
+  return (int64_t)n_frames * ((out_h + rb - 1) / rb) * ((out_w + kU8Cols - 1) / kU8Cols);
+}
+// KV_U8 covers windows of <= kU8MaxTaps taps on both axes (downscales <= 15.5x); beyond: VP_EUNSUPPORTED
+__host__ __device__ __forceinline__ bool u8_supported(int in_h, int in_w, int out_h, int out_w) {
+  const double fs = fmax(fmax((double)in_h / out_h, (double)in_w / out_w), 1.0);
+  return 4.0 * fs + 2.0 <= (double)kU8MaxTaps;
+}
+
+__host__ __device__ __forceinline__ int select_variant(int in_h, int in_w, int out_h, int out_w, int p,
+                                                       int resize_mode = 0) {
+  if (resize_mode == 1) return KV_U8;                    // VP_RESIZE_U8: the HF drop-in integer resize (N1)
   if (in_h == out_h && in_w == out_w && (p & 1) == 0) return KV_COPY;
   if (in_h >= out_h && in_w >= out_w && (p & 1) == 0 && in_h <= kTabInH && out_h <= kTabOutH &&
       pair_union_bound(in_w, out_w) <= kTeamUL) {

@@ -175,8 +175,8 @@ __device__ __forceinline__ int vfind(const VIdx& vx, int cnt, int64_t item) {   
   return lo;
 }
 
-// Per-variant work-index slots (variant_index_kernel): MILD, MEDIUM, STRONG, COPY, TEAM, WIDE, TEAML.
-constexpr int kNSlots = 7;
+// Per-variant work-index slots (variant_index_kernel): MILD, MEDIUM, STRONG, COPY, TEAM, WIDE, TEAML, U8.
+constexpr int kNSlots = 8;
 
 // Caller workspace of vp_resize_normalize_patchify (resize_ws_layout): the per-variant work index and the
 // KV_TEAM per-clip tables.  Nothing persists between calls.
@@ -189,6 +189,7 @@ struct ResizeWs {
   int* tflag;         // [n]  table flags (a non-negligible 5th live row)
   float4* vtab;       // [n][kTabInH]
   int* y1tab;         // [n][kTabOutH]
+  int2* u8prec;       // [n]  KV_U8 coefficient precision (horizontal, vertical)
 };
 ResizeWs resize_ws_layout(int n, void* base);
 VIdx ws_vidx(const ResizeWs& w, int n, int slot);
@@ -203,5 +204,8 @@ cudaError_t launch_fast_variants(const FKParams& kp, const vp_clip_plan* plans, 
                                  int64_t icap, void* pvv, int64_t vcap, int dev, int num_sms, unsigned mask,
                                  cudaStream_t s);
 FKParams make_fkparams(const vp_params* p);
+cudaError_t launch_u8(const FKParams& kp, const vp_clip_plan* plans, int n, const ResizeWs& w, const uint8_t* frames,
+                      const int64_t* coff, const int64_t* pitch, void* pi, int64_t icap, void* pvv, int64_t vcap,
+                      int num_sms, cudaStream_t s);
 
 }  // namespace vp

@@ -144,10 +144,12 @@ plan_kernel(vp_params P, const vp_clip_desc* __restrict__ clips, int n, vp_clip_
       v[r.is_image ? S_IMGTOK : S_VIDTOK] = patches / m2;
       v[r.is_image ? S_NIMG : S_NVID] = 1;
       v[S_GROUPS] = r.is_image ? 0 : r.gt;
-      const int kv = select_variant(clips[k].height, clips[k].width, r.out_h, r.out_w, P.patch_size);
+      const int kv = select_variant(clips[k].height, clips[k].width, r.out_h, r.out_w, P.patch_size, P.resize_mode);
       r.variant = kv;
       atomicOr(&s_variants, 1 << kv);
-      if (kv == KV_COPY) {
+      if (kv == KV_U8) {
+        v[S_TILES] = u8_tiles(r.n, clips[k].height, r.out_h, r.out_w);
+      } else if (kv == KV_COPY) {
         v[S_TILES] = (int64_t)r.n * (r.gh / P.merge_size) * copy_wchunks(r.gw, P.merge_size);
       } else if (kv == KV_TEAM || kv == KV_WIDE || kv == KV_TEAML) {
         v[S_TILES] = (int64_t)r.n *

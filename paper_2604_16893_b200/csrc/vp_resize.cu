@@ -333,6 +333,7 @@ __global__ void grids_kernel(const vp_clip_plan* __restrict__ plans, int n, int6
       const int64_t rows = (int64_t)pl.grid_t * pl.grid_h * pl.grid_w;
       const bool img = pl.is_image;
       if (!(img ? has_img : has_vid) || pl.patch_offset + rows > (img ? img_cap : vid_cap)) st = VP_ECAPACITY;
+      if (pl.kernel_variant == KV_U8 && !u8_supported(pl.in_h, pl.in_w, pl.out_h, pl.out_w)) st = VP_EUNSUPPORTED;
       int64_t* gptr = img ? img_grid : vid_grid;
       if (gptr != nullptr) {
         gptr[3 * pl.grid_index + 0] = pl.grid_t;
@@ -414,13 +415,16 @@ extern "C" vp_status vp_resize_normalize_patchify(const vp_params* p, const vp_c
   auto has = [&](int kv) { return (mask >> kv) & 1u; };
   const int fast_aligned = (reinterpret_cast<uintptr_t>(frames) & 15) == 0;
   const bool any_fast = has(vp::KV_MILD) || has(vp::KV_MEDIUM) || has(vp::KV_STRONG) || has(vp::KV_COPY) ||
-                        has(vp::KV_TEAM) || has(vp::KV_WIDE) || has(vp::KV_TEAML);
+                        has(vp::KV_TEAM) || has(vp::KV_WIDE) || has(vp::KV_TEAML) || has(vp::KV_U8);
   if (fast_aligned && any_fast) {
     const vp::FKParams fk = vp::make_fkparams(p);
     cudaError_t e = vp::launch_index(plans, n, clip_byte_offset, row_pitch, ws, s);
     if (e == cudaSuccess && (has(vp::KV_TEAM) || has(vp::KV_WIDE) || has(vp::KV_TEAML)))
       e = vp::launch_team(fk, plans, n, ws, frames, clip_byte_offset, row_pitch, pixel_values_images, img_rows_cap,
                           pixel_values_videos, vid_rows_cap, clip_status, dev, sms, mask, s);
+    if (e == cudaSuccess && has(vp::KV_U8))
+      e = vp::launch_u8(fk, plans, n, ws, frames, clip_byte_offset, row_pitch, pixel_values_images, img_rows_cap,
+                        pixel_values_videos, vid_rows_cap, sms, s);
     if (e == cudaSuccess)
       e = vp::launch_fast_variants(fk, plans, n, ws, frames, clip_byte_offset, row_pitch, pixel_values_images,
                                    img_rows_cap, pixel_values_videos, vid_rows_cap, dev, sms, mask, s);

@@ -566,7 +566,7 @@ team_vtab_kernel(const vp_clip_plan* __restrict__ plans, const int64_t* __restri
 // belongs to: the clips of a run share one vertical table.
 constexpr int kIdxThreads = 1024;
 __device__ __forceinline__ int variant_slot(int kv) {
-  return kv == KV_COPY ? 3 : (kv == KV_TEAM ? 4 : (kv == KV_WIDE ? 5 : (kv == KV_TEAML ? 6 : (kv <= KV_STRONG ? kv : -1))));
+  return kv == KV_COPY ? 3 : (kv == KV_TEAM ? 4 : (kv == KV_WIDE ? 5 : (kv == KV_TEAML ? 6 : (kv == KV_U8 ? 7 : (kv <= KV_STRONG ? kv : -1)))));
 }
 
 __global__ void __launch_bounds__(kIdxThreads)
@@ -711,6 +711,7 @@ ResizeWs resize_ws_layout(int n, void* base) {
   const size_t o_flag = take((size_t)n * sizeof(int));
   const size_t o_vtab = take((size_t)n * kTabInH * sizeof(float4));
   const size_t o_y1 = take((size_t)n * kTabOutH * sizeof(int));
+  const size_t o_u8 = take((size_t)n * sizeof(int2));
   w.bytes = o;
   char* b = reinterpret_cast<char*>(base);
   if (b != nullptr) {
@@ -721,6 +722,7 @@ ResizeWs resize_ws_layout(int n, void* base) {
     w.tflag = reinterpret_cast<int*>(b + o_flag);
     w.vtab = reinterpret_cast<float4*>(b + o_vtab);
     w.y1tab = reinterpret_cast<int*>(b + o_y1);
+    w.u8prec = reinterpret_cast<int2*>(b + o_u8);
   }
   return w;
 }

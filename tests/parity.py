@@ -18,7 +18,7 @@ def oracle_params(vp_params) -> dict:
                 patch_size=p.patch_size, merge_size=p.merge_size, video_max_pixels=p.video_max_pixels,
                 image_max_pixels=p.image_max_pixels, min_pixels=p.min_pixels, budget_mode=p.budget_mode,
                 sampling=p.sampling, mean=tuple(p.mean), std=tuple(p.std), out_dtype=p.out_dtype,
-                min_frames=p.min_frames)
+                min_frames=p.min_frames, resize_mode=p.resize_mode)
 
 
 def _ord_bf16(bits: np.ndarray) -> np.ndarray:

@@ -189,3 +189,30 @@ def test_column_pair_union_bound():
             ws.append((x0 + nz[0], x0 + nz[-1] + 1))
         for j in range(0, len(ws) - 1, 2):
             assert ws[j + 1][1] - ws[j][0] <= limit[var], (inn, out, j)
+
+
+def test_u8_resize_matches_torch_uint8_antialias():
+    """N1 oracle pin: resize_frame_u8 == torch.nn.functional.interpolate(uint8, bicubic, antialias=True) bit for bit
+    (the path HF's fast image / video processors take for uint8 frames), over down- and upscales, identity axes,
+    ragged sizes and the cfg2 geometry (720p -> 384x672)."""
+    import torch
+    import torch.nn.functional as F
+    rng = np.random.default_rng(11)
+    shapes = [(720, 1280, 384, 672), (37, 53, 20, 30), (64, 96, 64, 40), (50, 50, 50, 30), (30, 40, 60, 80),
+              (1, 7, 3, 2)] + [tuple(int(v) for v in rng.integers(1, 90, 4)) for _ in range(60)]
+    for H, W, oh, ow in shapes:
+        img = rng.integers(0, 256, (H, W, 3), dtype=np.uint8)
+        ref = F.interpolate(torch.from_numpy(img).permute(2, 0, 1)[None], size=(oh, ow), mode="bicubic",
+                            antialias=True)[0].permute(1, 2, 0).numpy()
+        assert np.array_equal(O.resize_frame_u8(img, oh, ow), ref), (H, W, oh, ow)
+
+
+def test_u8_resize_quantised_weights_sum():
+    """Each quantised row of coefficients sums to 2^p within its rounding (|sum - 2^p| <= taps/2): the integer
+    filter preserves a constant image up to rounding."""
+    for inn, out in ((720, 384), (1280, 672), (30, 80), (7, 3)):
+        q, p = O.quantize_weights_u8(inn, out)
+        for _, c in q:
+            assert abs(sum(c) - (1 << p)) <= len(c) / 2 + 1
+        img = np.full((inn, 5, 3), 200, np.uint8)
+        assert np.abs(O.resize_frame_u8(img, out, 5).astype(int) - 200).max() <= 1
