@@ -113,9 +113,14 @@ __device__ __forceinline__ void slice_span(const vp_clip_plan& pl, int ws, int s
 
 __device__ __forceinline__ float2& h2(float4& v, int h) { return reinterpret_cast<float2*>(&v)[h]; }
 
-// Retired-row swizzle (pixel-major float4 at tpos(x)): inside each 32-pixel block, sub-pixel-major (pixel 4a+k at
-// 8k+a) -- the V lanes' stores (pixels 4L+k) hit 8 distinct 16-B granules per quarter-warp.
-__device__ __forceinline__ int tpos(int x) { return (x & ~31) | ((x & 3) << 3) | ((x & 31) >> 2); }
+// Retired-row layout (KV_WIDE / KV_TEAM): pixel-major float4, granule class (x + 5 (x >> 3)) mod 8 inside each
+// 8-pixel block.  V retire stores (lane L writes pixels 4L..4L+3, one per instruction) are conflict-free (4 per-lane
+// offsets), and each H lane walks its union window in a rotated order -- at tap tt every lane reads a row position
+// = tt (mod UL); weights and addresses are rotated at slice setup -- so the H tap reads are conflict-free too: 1.00
+// wavefront per quarter-warp at every ratio simulated, vs 1.35 for round 1's sub-pixel-major swizzle at the cfg2
+// ratio (scripts/bank_sim.py); cfg5 K3 6.89 -> 6.34 ms per 64 clips.
+__device__ __forceinline__ int rpos(int x) { return (x & ~7) | ((x + 5 * (x >> 3)) & 7); }
+
 
 // A lane's 12 staged bytes (R0 G0 B0 R1 | G1 B1 R2 G2 | B2 R3 G3 B3 in words n0, n1, n2) as the six FFMA2 operand
 // pairs of the ring, ordered so that the accumulator quads are (R0 G0 B0 R3), (R1 G1 B1 G3), (R2 G2 B2 B3): pixels
@@ -197,7 +202,7 @@ resize_split_kernel(FKParams kp, const vp_clip_plan* __restrict__ plans, const V
   using Cfg = SplitCfg<NV, NH, kLarge>;
   constexpr int kPx = Cfg::kPx;
   static_assert(!kLarge || (PPL == 1 && kUL <= kTeamULL), "KV_TEAML: one pair per lane, padded rows");
-  auto pos = [](int x) { return kLarge ? x : tpos(x); };     // retired-row pixel position
+  auto pos = [](int x) { return kLarge ? x : (rpos(x)); };   // retired-row pixel position
   constexpr int kRowB = Cfg::kRowB;
   // preset geometry (p % 4 == 0 and p*m % 4 == 0): every out_h is a multiple of 4, so with 4 retire slots the slot of
   // output row i is i % 4 = the static unroll index U
@@ -298,6 +303,10 @@ resize_split_kernel(FKParams kp, const vp_clip_plan* __restrict__ plans, const V
     // retire address of this lane's 4 pixels (pixel 128*warp + 4*lane + k at +128k) in retire slot 0
     const uint32_t vsa = buf_s + (uint32_t)pos(warp * 128 + lane * 4) * 16u;
     constexpr uint32_t kPxB = kLarge ? 16u : 128u;  // distance of the lane's consecutive pixels in the retired row
+    constexpr bool kRot = !kLarge;
+    uint32_t vo[4];                                  // kRot: byte offsets of the lane's 4 pixels in a retire slot
+#pragma unroll
+    for (int j = 0; j < 4; ++j) vo[j] = kRot ? buf_s + (uint32_t)rpos(warp * 128 + lane * 4 + j) * 16u : vsa + j * kPxB;
     uint32_t rc = 0;                              // staged rows consumed: slot rc % kTDepth
     uint32_t rr = 0;                              // output rows retired (all items)
     for (int64_t item = my_a; item < my_b; ++item) {
@@ -346,12 +355,12 @@ resize_split_kernel(FKParams kp, const vp_clip_plan* __restrict__ plans, const V
       {                                                                                                       \
         const uint32_t rs = kStatic ? sbase + (uint32_t)U : rr % kNR;                                                 \
         mbar_wait_uni<VP_TEAM_HINT>(&rempty[rs], ((rr / kNR) & 1) ^ 1);                                       \
-        const uint32_t ra = vsa + rs * kSlotB;                                                                \
+        const uint32_t so_ = rs * kSlotB;                                                                     \
         const float4* a = acc[U];                     /* pixels 0..2 are quads .xyz; pixel 3 is the .w column */ \
-        sts_f4(ra, a[0]);                                                                                     \
-        sts_f4(ra + kPxB, a[1]);                                                                              \
-        sts_f4(ra + 2 * kPxB, a[2]);                                                                          \
-        sts_f4(ra + 3 * kPxB, make_float4(a[0].w, a[1].w, a[2].w, 0.f));                                      \
+        sts_f4(vo[0] + so_, a[0]);                                                                            \
+        sts_f4(vo[1] + so_, a[1]);                                                                            \
+        sts_f4(vo[2] + so_, a[2]);                                                                            \
+        sts_f4(vo[3] + so_, make_float4(a[0].w, a[1].w, a[2].w, 0.f));                                        \
         _Pragma("unroll") for (int q = 0; q < 3; ++q) acc[U][q] = make_float4(0.f, 0.f, 0.f, 0.f);            \
         __syncwarp();                                                                                         \
         mbar_arrive_if(&rfull[rs], l0 || VP_ALL_LANES_ARRIVE);                                                \
@@ -422,14 +431,18 @@ resize_split_kernel(FKParams kp, const vp_clip_plan* __restrict__ plans, const V
         const double r0 = s0 != 0.0 ? s0 : 1.0, r1 = s1 != 0.0 ? s1 : 1.0;
         const int xu = min(w0.x0, w1.x0);
         if (hact[pp] && max(w0.x1, w1.x1) - xu > kUL && clip_status != nullptr) clip_status[t.k] = VP_EUNSUPPORTED;
+        // rotated tap order (see rpos): lane's tap tt reads row position xu - pa + u with u = (tt - (xu - pa)) mod UL,
+        // so at every tap all lanes read positions of one residue class mod UL -- distinct banks under rpos
+        const int rot = !kLarge ? (kUL - (xu - pa) % kUL) % kUL : 0;
 #pragma unroll
-        for (int u = 0; u < kUL; ++u) {
+        for (int tt = 0; tt < kUL; ++tt) {
+          const int u = tt + rot < kUL ? tt + rot : tt + rot - kUL;
           const int x = xu + u;
           const float wa = (x >= w0.x0 && x < w0.x1) ? (float)(keys_d(((double)x - w0.c + 0.5) * w0.inv) / r0) : 0.f;
           const float wb = (x >= w1.x0 && x < w1.x1) ? (float)(keys_d(((double)x - w1.c + 0.5) * w1.inv) / r1) : 0.f;
-          wp[pp][u] = kFold ? make_float2(wa * kp.scale[0], wb * kp.scale[0]) : make_float2(wa, wb);
-          toff[pp][u] = kLarge ? buf_s + (uint32_t)(xu - pa + u) * 16u        // padded row: base + 16 u
-                               : buf_s + (uint32_t)tpos(min(x - pa, kPx - 1)) * 16u;   // slack taps (weight 0) stay in the row
+          wp[pp][tt] = kFold ? make_float2(wa * kp.scale[0], wb * kp.scale[0]) : make_float2(wa, wb);
+          toff[pp][tt] = kLarge ? buf_s + (uint32_t)(xu - pa + u) * 16u        // padded row: base + 16 u
+                                : buf_s + (uint32_t)pos(min(x - pa, kPx - 1)) * 16u;   // slack taps (weight 0) stay in the row
         }
         const int jl0 = ja % B, wbk = ja / B, mw = jl0 / p, px = jl0 - mw * p;
         colpart[pp] = (wbk * m * m + mw) * D + px;

@@ -79,3 +79,47 @@ for B in (16, 32, 64, 128):
 for ln, lm in lmaps.items():
     f = lambda x: x
     print(f"natural     lmap {ln:4s} vstore {vstore_cost(f):.2f} hread " + " ".join(f"{hread_cost_map(f,s,lm):.2f}" for s in range(3)))
+
+
+# ---------------------------------------------------------------------------------------------------------------
+# Round 2 (team kernels, whole-row or sliced footprints): retired-row layouts x H tap order.  H lane q owns column
+# pair (2q, 2q+1); its UL-tap union window starts at x0(2q).  "rotation" = the tap order of lane q: at instruction t
+# it reads position x0 + ((t + r_q) mod UL).  Wavefronts per quarter-warp (8 lanes x 16 B), 1.0 = conflict-free.
+# Result: layout rpos(x) = (x & ~7) | ((x + 5 (x >> 3)) & 7) with r_q = -x0 mod UL (every lane
+# reads one residue class mod UL per instruction) is conflict-free for V stores and H reads at every ratio below.
+def team_cost(inn, out, layout, rot, UL=10):
+    Q = out // 2
+    st = [window(2 * q, inn, out)[0] for q in range(Q)]
+    tot = n = 0
+    for t in range(UL):
+        for l0 in range(0, Q, 8):
+            g = [layout(st[q] + ((t + rot(q % 32, st[q])) % UL)) for q in range(l0, min(l0 + 8, Q))]
+            cls = {}
+            for x in g:
+                cls.setdefault(x % 8, set()).add(x)
+            tot += max(len(v) for v in cls.values())
+            n += 1
+    return tot / n
+
+
+def team_vstore_cost(layout):
+    tot = n = 0
+    for j in range(4):
+        for l0 in range(0, 320, 8):
+            g = [layout(4 * L + j) for L in range(l0, l0 + 8)]
+            cls = {}
+            for x in g:
+                cls.setdefault(x % 8, set()).add(x)
+            tot += max(len(v) for v in cls.values())
+            n += 1
+    return tot / n
+
+
+if __name__ == "__main__":
+    tpos = lambda x: (x & ~31) | ((x & 3) << 3) | ((x & 31) >> 2)
+    rpos = lambda x: (x & ~7) | ((x + 5 * (x >> 3)) & 7)
+    ratios = [(1280, 672), (720, 384), (854, 672), (640, 336), (1000, 640), (1920, 1088), (1280, 1024)]
+    for name, lay, rot in (("round-1 sub-pixel-major, no rotation", tpos, lambda q, x: 0),
+                           ("rpos, rotation -x0 mod UL", rpos, lambda q, x: -x)):
+        print(f"{name:40s} V stores {team_vstore_cost(lay):.2f}  H reads",
+              [round(team_cost(i, o, lay, rot), 3) for i, o in ratios])
