@@ -58,4 +58,20 @@ for dtype in (0, 1):
     one(pre, mixed, pad=1)
     big = vp.VisualPreprocessor(image_max_pixels=1024, video_max_pixels=1024, max_frames=3, out_dtype=dtype)
     one(big, [I.image(2000, 3000), I.clip(3, 2.0, 1500, 2600)])
+# the round-2 kernels: u8 HF drop-in resize + linspace sampling, dedup/views, NV12 intake, vision ids, presets
+u8 = vp.VisualPreprocessor(max_frames=4, video_max_pixels=20000, image_max_pixels=30000, resize_mode=vp.VP_RESIZE_U8,
+                           sampling=vp.VP_SAMPLE_LINSPACE)
+one(u8, [I.clip(9, 2.0, 120, 200), I.image(90, 60), I.image(2000, 3000)])
+q25 = vp.VisualPreprocessor.from_preset("qwen2_5_vl", max_frames=8, video_max_pixels=50176)
+plq = q25.plan([I.clip(300, 29.97, 360, 640), I.clip(50, 10.0, 224, 224)])
+q25.second_per_grid(plq)
+uc, ul, uid = pre.dedup(mixed, [k // 2 for k in range(len(mixed))])
+upl = pre.plan(uc)
+pre.views(upl, uid)
+H, W, n = 24, 40, 2
+nv = torch.randint(0, 256, (n * H * 3 // 2 * W,), dtype=torch.uint8, device="cuda")
+rgb = torch.empty(n * H * 3 * W, dtype=torch.uint8, device="cuda")
+vp.nv12_to_rgb(nv, nv[H * W:], W, H * 3 // 2 * W, H, W, n, rgb, 3 * W, 3 * W * H)
+vp.vision_ids(torch.tensor([[2, 8, 12], [1, 4, 4]], dtype=torch.int64, device="cuda"), 2)
+torch.cuda.synchronize()
 print("sanitize_run OK")
