@@ -227,6 +227,11 @@ def run_ours(args, rank, world, local_rank):
         e2e = run_e2e(args, pre, pl, frames, off, pitch, out, tt, cu, pos, deltas, rst, ws, per, dev, world,
                       tokens_rank)
 
+    e2e_nv12 = None
+    if not args.no_e2e and args.config == "cfg5":
+        e2e_nv12 = run_e2e_nv12(args, pre, pl, frames, off, pitch, out, tt, cu, pos, deltas, rst, ws, per, dev,
+                                world, tokens_rank)
+
     # ---------------- N3: the same job with GRPO dedup (64 prompts x 8 rollouts, P:73 / P:271) ----------------
     dedup = None
     if not args.no_dedup and args.config == "cfg5":
@@ -258,6 +263,7 @@ def run_ours(args, rank, world, local_rank):
             "gpu_launches": launches_per_step * args.steps,
             "clocks": clk,
             "e2e": e2e,
+            "e2e_nv12": e2e_nv12,
             "dedup_64x8": dedup,
         }
     return result
@@ -492,6 +498,90 @@ def run_e2e(args, pre, pl, frames, off, pitch, out, tt, cu, pos, deltas, rst, ws
             "d2h_bytes_per_step": d2h, "ms_per_step": ms, "steps": args.e2e_steps,
             "path": "pinned host u8 frames -> H2D (copy stream, chunks of %d clips) overlapped with K3; "
                     "D2H of grids/status/deltas" % chunk}
+
+
+def run_e2e_nv12(args, pre, pl, frames, off, pitch, out, tt, cu, pos, deltas, rst, ws, per, dev, world, tokens_rank):
+    """As run_e2e, but the host holds what a decoder emits -- NV12 (Y plane + interleaved UV, 1.5 B/pixel) -- and
+    the device converts it with vp_nv12_to_rgb (N4) straight into each clip's slot of the K3 frame buffer: half
+    the PCIe bytes of RGB.  NV12 staging on the device is double-buffered per chunk of clips."""
+    import torch
+    import torch.distributed as dist
+    import paper_2604_16893_b200 as vp
+
+    P = pre.launch_params(pl)
+    ph = pl.plans_host
+    chunk = max(1, min(args.e2e_chunk, per))
+    n, H, W = int(ph["n_frames"][0]), int(ph["in_h"][0]), int(ph["in_w"][0])
+    fstride = H * W * 3 // 2
+    nv_clip = n * fstride
+    ring = max(chunk, min(2 * chunk, per))
+    host = torch.randint(0, 256, (ring * nv_clip,), dtype=torch.uint8).pin_memory()
+    stage = [torch.empty(chunk * nv_clip, dtype=torch.uint8, device=dev) for _ in range(2)]
+    st_h = torch.empty_like(out["clip_status"], device="cpu").pin_memory()
+    dl_h = torch.empty_like(deltas, device="cpu").pin_memory()
+    grids_h = torch.empty_like(out["video_grid_thw"], device="cpu").pin_memory()
+    rs_h = torch.empty_like(rst, device="cpu").pin_memory()
+    comp = torch.cuda.current_stream(dev)
+    copy = torch.cuda.Stream(dev)
+    ws_chunk = vp.resize_workspace(chunk, dev)
+    torch_off = torch.from_numpy(off).to(dev)
+    torch_pitch = torch.from_numpy(pitch).to(dev)
+    d2h = grids_h.numel() * 8 + st_h.numel() * 4 + dl_h.numel() * 8 + rs_h.numel() * 4
+
+    def step():
+        vp.plan_frames(P, pl.clips_dev, per, pl.plans_dev, pl.frame_indices, pl.totals_dev, pl.group_timestamps)
+        freed = [torch.cuda.Event(), torch.cuda.Event()]
+        for e in freed:
+            e.record(comp)
+        for ci, c0 in enumerate(range(0, per, chunk)):
+            c1 = min(per, c0 + chunk)
+            buf = stage[ci % 2]
+            with torch.cuda.stream(copy):
+                copy.wait_event(freed[ci % 2])      # the conversions of chunk ci-2 are done with this buffer
+                for k in range(c0, c1):
+                    src = host[(k % ring) * nv_clip: (k % ring + 1) * nv_clip]
+                    buf[(k - c0) * nv_clip: (k - c0 + 1) * nv_clip].copy_(src, non_blocking=True)
+                e = torch.cuda.Event()
+                e.record(copy)
+            comp.wait_event(e)
+            for k in range(c0, c1):
+                nb = buf[(k - c0) * nv_clip:]
+                vp.nv12_to_rgb(nb, nb[H * W:], W, fstride, H, W, n, frames[int(off[k]):], int(pitch[k]),
+                               H * int(pitch[k]), stream=comp)
+            fe = torch.cuda.Event()
+            fe.record(comp)
+            freed[ci % 2] = fe
+            vp.resize_normalize_patchify(P, pl.plans_dev, c1 - c0, frames, torch_off, torch_pitch, None,
+                                         out["pixel_values_videos"], out["image_grid_thw"], out["video_grid_thw"],
+                                         out["clip_status"], workspace=ws_chunk, stream=comp, first_clip=c0)
+        vp.rope_index(P, vp.VP_ROPE_QWEN3_SPLIT, tt, cu, None, out["video_grid_thw"], pos, deltas, rst, ws)
+        grids_h.copy_(out["video_grid_thw"], non_blocking=True)
+        st_h.copy_(out["clip_status"], non_blocking=True)
+        dl_h.copy_(deltas, non_blocking=True)
+        rs_h.copy_(rst, non_blocking=True)
+
+    for _ in range(max(1, args.warmup // 2)):
+        step()
+    torch.cuda.synchronize()
+    if world > 1:
+        dist.barrier()
+    a = torch.cuda.Event(enable_timing=True)
+    b = torch.cuda.Event(enable_timing=True)
+    a.record(comp)
+    for _ in range(args.e2e_steps):
+        step()
+    b.record(comp)
+    torch.cuda.synchronize()
+    ms = a.elapsed_time(b) / args.e2e_steps
+    t = torch.tensor([ms], dtype=torch.float64, device=dev)
+    if world > 1:
+        dist.all_reduce(t, op=dist.ReduceOp.MAX)
+    ms = float(t.item())
+    assert (st_h[:per].numpy() == 0).all()
+    return {"value": tokens_rank * world / (ms * 1e-3), "unit": UNIT, "h2d_bytes_per_step": per * nv_clip,
+            "d2h_bytes_per_step": d2h, "ms_per_step": ms, "steps": args.e2e_steps,
+            "path": "pinned host NV12 frames (decoder output) -> H2D (copy stream, double-buffered chunks of %d "
+                    "clips) -> vp_nv12_to_rgb into the K3 frame buffer -> K3; D2H of grids/status/deltas" % chunk}
 
 
 # ----------------------------------------------------------------------------------------------
