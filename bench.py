@@ -344,7 +344,8 @@ def k3_launches(mask: int, n: int) -> int:
     the team tables when team/wide clips are; one launch per present TMA variant; the direct kernel if needed."""
     has = lambda v: (mask >> v) & 1
     tma = [has(v) for v in (0, 1, 2, 4, 5, 6, 8)]       # mild, medium, strong, copy, team, wide, team-large
-    n_l = 2 + (1 if any(tma) else 0) + sum(tma) + (1 if (has(5) or has(6) or has(8)) else 0) + has(7)
+    n_l = (2 + (1 if (any(tma) or has(9)) else 0) + sum(tma) + (1 if (has(5) or has(6) or has(8)) else 0) + has(7)
+           + 2 * has(9))                                 # + direct; + u8 precision and u8 tiles
     return n_l if n > 0 else 0
 
 

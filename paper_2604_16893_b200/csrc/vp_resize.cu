@@ -111,7 +111,7 @@ resize_generic_kernel(KParams kp, const vp_clip_plan* __restrict__ plans, int n,
    if (kk < n) {
      const vp_clip_plan& q = plans[kk];
      const bool fast_ok = fast_aligned && q.kernel_variant != KV_GENERIC && ((clip_off[kk] | pitch_arr[kk]) & 15) == 0;
-     if (q.status == VP_OK && !fast_ok && q.kernel_variant != KV_DIRECT)
+     if (q.status == VP_OK && !fast_ok && q.kernel_variant != KV_DIRECT && q.kernel_variant != KV_U8)
        my_tiles = clip_tiles(q.grid_t, q.grid_h, q.grid_w, kp.m);
    }
    // block exclusive scan of (my_tiles, owned)
@@ -415,17 +415,17 @@ extern "C" vp_status vp_resize_normalize_patchify(const vp_params* p, const vp_c
   auto has = [&](int kv) { return (mask >> kv) & 1u; };
   const int fast_aligned = (reinterpret_cast<uintptr_t>(frames) & 15) == 0;
   const bool any_fast = has(vp::KV_MILD) || has(vp::KV_MEDIUM) || has(vp::KV_STRONG) || has(vp::KV_COPY) ||
-                        has(vp::KV_TEAM) || has(vp::KV_WIDE) || has(vp::KV_TEAML) || has(vp::KV_U8);
-  if (fast_aligned && any_fast) {
+                        has(vp::KV_TEAM) || has(vp::KV_WIDE) || has(vp::KV_TEAML);
+  if ((fast_aligned && any_fast) || has(vp::KV_U8)) {
     const vp::FKParams fk = vp::make_fkparams(p);
     cudaError_t e = vp::launch_index(plans, n, clip_byte_offset, row_pitch, ws, s);
-    if (e == cudaSuccess && (has(vp::KV_TEAM) || has(vp::KV_WIDE) || has(vp::KV_TEAML)))
+    if (e == cudaSuccess && fast_aligned && (has(vp::KV_TEAM) || has(vp::KV_WIDE) || has(vp::KV_TEAML)))
       e = vp::launch_team(fk, plans, n, ws, frames, clip_byte_offset, row_pitch, pixel_values_images, img_rows_cap,
                           pixel_values_videos, vid_rows_cap, clip_status, dev, sms, mask, s);
     if (e == cudaSuccess && has(vp::KV_U8))
       e = vp::launch_u8(fk, plans, n, ws, frames, clip_byte_offset, row_pitch, pixel_values_images, img_rows_cap,
                         pixel_values_videos, vid_rows_cap, sms, s);
-    if (e == cudaSuccess)
+    if (e == cudaSuccess && fast_aligned)
       e = vp::launch_fast_variants(fk, plans, n, ws, frames, clip_byte_offset, row_pitch, pixel_values_images,
                                    img_rows_cap, pixel_values_videos, vid_rows_cap, dev, sms, mask, s);
     if (e != cudaSuccess) {

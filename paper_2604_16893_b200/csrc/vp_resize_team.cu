@@ -602,7 +602,9 @@ variant_index_kernel(const vp_clip_plan* __restrict__ plans, int n, const int64_
     int64_t items = 0;
     if (k < n) {
       const vp_clip_plan& pl = plans[k];
-      if (pl.status == VP_OK && pl.tile_count > 0 && ((coff[k] | pitch[k]) & 15) == 0) {
+      // TMA variants need 16-B aligned rows; the u8 kernel reads bytes and takes any alignment
+      if (pl.status == VP_OK && pl.tile_count > 0 &&
+          (pl.kernel_variant == KV_U8 || ((coff[k] | pitch[k]) & 15) == 0)) {
         slot = variant_slot(pl.kernel_variant);
         items = pl.tile_count;
       }

@@ -68,3 +68,24 @@ def test_u8_mode_unsupported_ratio():
     assert out["clip_status"][:2].cpu().tolist() == [vp.VP_EUNSUPPORTED, 0]
     with pytest.raises(vp.VpError):
         pre.run(pl, *pack_frames(fl, [(3 * c["width"] + 15) // 16 * 16 for c in clips]))
+
+
+def test_u8_mode_any_alignment():
+    """The u8 kernel reads bytes: clips with unaligned pitches, and a frame buffer whose base is not 16-B aligned,
+    still take it (not the float generic kernel)."""
+    import paper_2604_16893_b200 as vp
+    pre = vp.VisualPreprocessor(max_frames=3, video_max_pixels=20000, image_max_pixels=30000, out_dtype=1,
+                                resize_mode=vp.VP_RESIZE_U8)
+    clips = [I.clip(7, 2.0, 70, 100), I.image(90, 61), I.image(33, 257)]
+    pl = pre.plan(clips)
+    op = oracle_params(pre.params)
+    oplans, _ = O.plan_batch(op, clips)
+    fl = host_frames(oplans)
+    buf, offs, pit = pack_frames(fl, [3 * c["width"] + 1 for c in clips])           # unaligned pitches
+    shifted = torch.zeros(buf.numel() + 3, dtype=torch.uint8, device="cuda")
+    shifted[3:] = buf                                                                  # base off by 3 bytes
+    out = pre.run(pl, shifted[3:], offs, pit)
+    torch.cuda.synchronize()
+    ref = O.process_batch(op, clips, fl, plans=oplans)
+    assert_pixels(out["pixel_values"].cpu(), ref["pixel_values_images"], "images")
+    assert_pixels(out["pixel_values_videos"].cpu(), ref["pixel_values_videos"], "videos")
