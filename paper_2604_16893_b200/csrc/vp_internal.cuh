@@ -117,7 +117,8 @@ constexpr int kWideNV = 10, kWideNH = 6, kWidePPL = 2;
 constexpr int kTeamUL = 10;       // union taps of a column pair (registers)
 constexpr int kTeamULL = 32;      // KV_TEAML: union taps of a column pair for large downscales (unswizzled rows)
 constexpr int kTabInH = 2176;     // per-clip vertical weight records (float4 per source row)
-constexpr int kTabOutH = 1088;    // per-clip window ends (int per output row, padded to a multiple of 4)
+constexpr int kTabOutH = 1088;    // per-clip window ends (int per output row)
+constexpr int kTabOutStride = kTabOutH + 4;   // + 4 sentinel entries past the last output row
 
 struct TeamGeo {
   int ws, nslices;                // slice width (columns), slices per frame; ws = 0: does not fit

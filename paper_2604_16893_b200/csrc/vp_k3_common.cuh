@@ -188,7 +188,7 @@ struct ResizeWs {
   int* alias;         // [n]  clip -> first clip of its run of equal (in_h, out_h) TEAM / WIDE clips (table owner)
   int* tflag;         // [n]  table flags (a non-negligible 5th live row)
   float4* vtab;       // [n][kTabInH]
-  int* y1tab;         // [n][kTabOutH]
+  int* y1tab;         // [n][kTabOutStride]
   int2* u8prec;       // [n]  KV_U8 coefficient precision (horizontal, vertical)
 };
 ResizeWs resize_ws_layout(int n, void* base);

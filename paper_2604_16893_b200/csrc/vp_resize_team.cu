@@ -28,6 +28,7 @@
 // share one table.
 #include "vp_k3_common.cuh"
 #include <atomic>
+#include <type_traits>
 
 namespace vp {
 namespace {
@@ -132,25 +133,28 @@ __device__ __forceinline__ float byte_magic(uint32_t w, int k) {      // 2^23 + 
 }
 __device__ __forceinline__ void cvt_ring(uint32_t n0, uint32_t n1, uint32_t n2, float2 (&f)[6]) {
   const float2 mm = make_float2(-8388608.f, -8388608.f);
+#if defined(VP_EXP_NOI2F)
+  f[0] = __fadd2_rn(make_float2(byte_magic(n0, 0), byte_magic(n0, 1)), mm);
+  f[1] = __fadd2_rn(make_float2(byte_magic(n0, 2), byte_magic(n2, 1)), mm);
+  f[2] = __fadd2_rn(make_float2(byte_magic(n0, 3), byte_magic(n1, 0)), mm);
+  f[3] = __fadd2_rn(make_float2(byte_magic(n1, 1), byte_magic(n2, 2)), mm);
+  f[4] = __fadd2_rn(make_float2(byte_magic(n1, 2), byte_magic(n1, 3)), mm);
+  f[5] = __fadd2_rn(make_float2(byte_magic(n2, 0), byte_magic(n2, 3)), mm);
+#elif defined(VP_EXP_ALLI2F)
+  f[0] = make_float2(byte_i2f(n0, 0), byte_i2f(n0, 1));
+  f[1] = make_float2(byte_i2f(n0, 2), byte_i2f(n2, 1));
+  f[2] = make_float2(byte_i2f(n0, 3), byte_i2f(n1, 0));
+  f[3] = make_float2(byte_i2f(n1, 1), byte_i2f(n2, 2));
+  f[4] = make_float2(byte_i2f(n1, 2), byte_i2f(n1, 3));
+  f[5] = make_float2(byte_i2f(n2, 0), byte_i2f(n2, 3));
+#else
   f[0] = make_float2(byte_i2f(n0, 0), byte_i2f(n0, 1));                                   // R0 G0
   f[1] = __fadd2_rn(make_float2(byte_magic(n0, 2), byte_magic(n2, 1)), mm);               // B0 R3
   f[2] = make_float2(byte_i2f(n0, 3), byte_i2f(n1, 0));                                   // R1 G1
   f[3] = __fadd2_rn(make_float2(byte_magic(n1, 1), byte_magic(n2, 2)), mm);               // B1 G3
   f[4] = make_float2(byte_i2f(n1, 2), byte_i2f(n1, 3));                                   // R2 G2
   f[5] = make_float2(byte_i2f(n2, 0), byte_i2f(n2, 3));                                   // B2 B3
-}
-
-// One source row into the ring: output rows i..i+3 (i in slot U) get weights w.x..w.w.
-template <int U>
-__device__ __forceinline__ void ring4(float4 (&acc)[4][3], const float4 w, const float2 (&f)[6]) {
-  const float ws[4] = {w.x, w.y, w.z, w.w};
-#pragma unroll
-  for (int r = 0; r < 4; ++r) {
-    const int slot = (U + r) & 3;
-    const float2 ww = make_float2(ws[r], ws[r]);
-#pragma unroll
-    for (int q = 0; q < 6; ++q) h2(acc[slot][q >> 1], q & 1) = __ffma2_rn(ww, f[q], h2(acc[slot][q >> 1], q & 1));
-  }
+#endif
 }
 
 // normalise (O6) as FFMA2 over the column pair, clamp (C12) in the output domain (clamp(v,0,255)*s+b ==
@@ -183,6 +187,9 @@ __device__ __forceinline__ void store_pair(const FKParams& kp, char* q, float2 a
       else *reinterpret_cast<uint32_t*>(d + (int64_t)c * cstride * kEsz) = o[c].x;
     }
   };
+#ifdef VP_EXP_NOSTG
+  if (o[0].x == 0x7fc17fc1u)
+#endif
   put(q);
   if (nslots > 1) {                                // frame n-1 also fills the temporal pad slots (O7)
     for (int s2 = 1, ti = ti0; s2 < nslots; ++s2) {
@@ -299,99 +306,171 @@ resize_split_kernel(FKParams kp, const vp_clip_plan* __restrict__ plans, const V
 
   if (warp < NV) {
     // ================================================================= V warps
+    // The source-row loop runs over whole staging groups (kTGrp rows, fully unrolled: static staging offsets, the
+    // group wait / refill once per group, and the next row's loads free to move above this row's FMAs).  Ring slot
+    // s holds the output rows i with i % 4 == s and the weight records are stored in slot order (team_vtab_kernel),
+    // so every row's FMAs use static slots; a row that completes output row i retires slot i % 4 (a switch, taken
+    // once per output row).
     const uint32_t stage_s = smem_u32(stage), wrec_s = smem_u32(wrec);
-    // retire address of this lane's 4 pixels (pixel 128*warp + 4*lane + k at +128k) in retire slot 0
-    const uint32_t vsa = buf_s + (uint32_t)pos(warp * 128 + lane * 4) * 16u;
     constexpr uint32_t kPxB = kLarge ? 16u : 128u;  // distance of the lane's consecutive pixels in the retired row
     constexpr bool kRot = !kLarge;
-    uint32_t vo[4];                                  // kRot: byte offsets of the lane's 4 pixels in a retire slot
+    uint32_t vo[4];                                  // retire addresses of the lane's 4 pixels in retire slot 0
+    {
+      const uint32_t vsa = buf_s + (uint32_t)pos(warp * 128 + lane * 4) * 16u;
 #pragma unroll
-    for (int j = 0; j < 4; ++j) vo[j] = kRot ? buf_s + (uint32_t)rpos(warp * 128 + lane * 4 + j) * 16u : vsa + j * kPxB;
-    uint32_t rc = 0;                              // staged rows consumed: slot rc % kTDepth
+      for (int j = 0; j < 4; ++j) vo[j] = kRot ? buf_s + (uint32_t)rpos(warp * 128 + lane * 4 + j) * 16u : vsa + j * kPxB;
+    }
+    float4 acc[4][3];
+#pragma unroll
+    for (int r = 0; r < 4; ++r)
+#pragma unroll
+      for (int q = 0; q < 3; ++q) acc[r][q] = make_float4(0.f, 0.f, 0.f, 0.f);
+    uint32_t rc = 0;                              // staged rows consumed (a multiple of kTGrp at every group start)
     uint32_t rr = 0;                              // output rows retired (all items)
-    for (int64_t item = my_a; item < my_b; ++item) {
+    int64_t item = my_a;
+    int in_h = 0, y = 0, i = 0, nend = 0, nnext = 0;
+    uint32_t lofs = 0;                            // byte offset of this lane's 12 bytes inside a staged row
+    const int* y1 = nullptr;
+    auto open = [&]() {                           // item `item`: its window ends and footprint offset
       const TItem t = decode_item<NV, NH * PPL>(vx, cnt, item, plans, p);
       const vp_clip_plan& pl = plans[t.k];
-      const int in_h = pl.in_h, out_h = pl.out_h;
+      in_h = pl.in_h;
       const int pa = window_of(pl.in_w, pl.out_w, t.s * t.ws).x0 & ~3;
-      const int* y1 = y1tab + (int64_t)tab_alias[t.k] * kTabOutH;
-      // byte offset of this lane's 12 bytes inside a staged row (the footprint starts at (3*pa) & 15)
-      const uint32_t lofs = (uint32_t)(((3 * pa) & 15) + 384 * warp + 12 * lane);
-      float4 acc[4][3];
+      y1 = y1tab + (int64_t)tab_alias[t.k] * kTabOutStride;
+      lofs = (uint32_t)(((3 * pa) & 15) + 384 * warp + 12 * lane);   // the footprint starts at (3*pa) & 15
+      y = 0;
+      i = 0;
+      nend = __ldg(y1);
+      nnext = __ldg(y1 + 1);
+    };
+    // retire output row i (ring slot C = i % 4) into retire slot rr % kNR.  Preset geometry (kStatic: every out_h is
+    // a multiple of 4, so rr % 4 == i % 4): the retire slot is C itself and its addresses are immediates.
+    auto retire = [&](float4 (&a)[3], auto cslot) {
+      constexpr int C = decltype(cslot)::value;
+      const uint32_t rs = kStatic ? (uint32_t)C : rr % kNR;
+      mbar_wait_uni<VP_TEAM_HINT>(&rempty[rs], ((rr / kNR) & 1) ^ 1);
+      const uint32_t so_ = rs * kSlotB;
+      sts_f4(vo[0] + so_, a[0]);                 // pixels 0..2 are quads .xyz; pixel 3 is the .w column
+      sts_f4(vo[1] + so_, a[1]);
+      sts_f4(vo[2] + so_, a[2]);
+      sts_f4(vo[3] + so_, make_float4(a[0].w, a[1].w, a[2].w, 0.f));
+      // clear the slot as a[q] * 0 (6 FMUL2; the accumulators are finite): ptxas materialises literal zeros here as
+      // 18 uniform-register moves
+      const float2 z2 = make_float2(0.f, 0.f);
 #pragma unroll
-      for (int r = 0; r < 4; ++r)
+      for (int q = 0; q < 3; ++q) {
+        h2(a[q], 0) = __fmul2_rn(h2(a[q], 0), z2);
+        h2(a[q], 1) = __fmul2_rn(h2(a[q], 1), z2);
+      }
+      __syncwarp();
+      mbar_arrive_if(&rfull[rs], l0 || VP_ALL_LANES_ARRIVE);
+      ++rr;
+    };
+    // one staged row (converted): FMA into the ring (static slots), retire the output rows it completes
+    auto fma_row = [&](const float2 (&fv)[6], const float4 wv) {
+      const float ws[4] = {wv.x, wv.y, wv.z, wv.w};
+#ifndef VP_EXP_NOV
 #pragma unroll
-        for (int q = 0; q < 3; ++q) acc[r][q] = make_float4(0.f, 0.f, 0.f, 0.f);
-      int y = 0;
-      // after the last row of group g: the last V warp to finish it refills it
-      auto group_done = [&](uint32_t g, uint32_t parity) {
-        if (VP_ALL_LANES_ARRIVE) mbar_arrive(&sread[g]);   // verification build: this lane's reads of g are done
-        __syncwarp();
-        int old = 0;
-        if (l0) {
-          __threadfence_block();
-          old = atomicAdd(&gcnt[g], 1);
-          if (old == NV - 1) gcnt[g] = 0;
+      for (int s = 0; s < 4; ++s) {
+        const float2 ww = make_float2(ws[s], ws[s]);
+#pragma unroll
+        for (int c = 0; c < 6; ++c) h2(acc[s][c >> 1], c & 1) = __ffma2_rn(ww, fv[c], h2(acc[s][c >> 1], c & 1));
+      }
+#else
+      h2(acc[0][0], 0) = __fadd2_rn(h2(acc[0][0], 0), __fadd2_rn(fv[0], fv[5]));   // keep the conversions alive
+      h2(acc[1][0], 0) = __fadd2_rn(h2(acc[1][0], 0), __fadd2_rn(fv[1], fv[4]));
+      h2(acc[2][0], 0) = __fadd2_rn(h2(acc[2][0], 0), __fadd2_rn(fv[2], fv[3]));
+      acc[3][0].x += ws[0] + ws[3];
+#endif
+      ++y;
+      while (y == nend) {                         // source row y-1 completed output row i (ring slot i % 4)
+        switch (i & 3) {
+          case 0: retire(acc[0], std::integral_constant<int, 0>{}); break;
+          case 1: retire(acc[1], std::integral_constant<int, 1>{}); break;
+          case 2: retire(acc[2], std::integral_constant<int, 2>{}); break;
+          default: retire(acc[3], std::integral_constant<int, 3>{}); break;
         }
-        if (__shfl_sync(0xffffffffu, old, 0) == NV - 1) {
-          if (VP_ALL_LANES_ARRIVE) mbar_wait_uni(&sread[g], parity);
-          issue_group(g);
+        ++i;
+        nend = nnext;
+        nnext = __ldg(y1 + i + 1);                // the sentinels past out_h end the chain
+      }
+    };
+    auto row = [&](uint32_t n0, uint32_t n1, uint32_t n2, float4 wv) {
+      float2 fv[6];
+      cvt_ring(n0, n1, n2, fv);
+      fma_row(fv, wv);
+    };
+    open();
+    for (;;) {
+      if (y == in_h) {                            // item done (all its output rows retired)
+        if (++item >= my_b) break;
+        open();
+      }
+      const uint32_t g = (rc / kTGrp) % kTNGrp;
+      const uint32_t par = (rc / kTDepth) & 1;
+      mbar_wait_uni(&sfull[g], par);
+      const uint32_t gst = stage_s + g * (kTGrp * kRowB);
+      const uint32_t gw = wrec_s + g * (kTGrp * 16);
+      bool fin = false;
+      if (in_h - y >= kTGrp) {
+        // the whole group belongs to this item: rows in pairs with two register sets, each row's bytes loaded one
+        // row and converted half a row ahead of its FMAs (the conversions of row q+1 overlap the FMAs of row q in
+        // one basic block); the look-ahead past the group wraps to its own consumed rows (no stray reads).
+        const uint32_t sb = gst + lofs;
+        auto ld3 = [&](int r, uint32_t& x0, uint32_t& x1, uint32_t& x2) {
+          const uint32_t sa = sb + (uint32_t)r * kRowB;
+          x0 = lds_u32(sa); x1 = lds_u32(sa + 4); x2 = lds_u32(sa + 8);
+        };
+        uint32_t ra0, ra1, ra2, rb0, rb1, rb2;
+        float2 fa[6], fb[6];
+        ld3(0, ra0, ra1, ra2);
+        float4 wa = lds_f4(gw);
+        ld3(1, rb0, rb1, rb2);
+        float4 wb = lds_f4(gw + 16);
+        cvt_ring(ra0, ra1, ra2, fa);
+#pragma unroll 1
+        for (int q = 0; q < kTGrp; q += 2) {
+          const int q2 = (q + 2) & (kTGrp - 1), q3 = (q + 3) & (kTGrp - 1);
+          cvt_ring(rb0, rb1, rb2, fb);
+          ld3(q2, ra0, ra1, ra2);
+          fma_row(fa, wa);
+          wa = lds_f4(gw + q2 * 16);
+          cvt_ring(ra0, ra1, ra2, fa);
+          ld3(q3, rb0, rb1, rb2);
+          fma_row(fb, wb);
+          wb = lds_f4(gw + q3 * 16);
         }
-      };
-#define VP_V_BODY(U)                                                                                         \
-      {                                                                                                       \
-        if ((rc & (kTGrp - 1)) == 0) mbar_wait_uni(&sfull[(rc / kTGrp) % kTNGrp], (rc / kTDepth) & 1);        \
-        const uint32_t slot = rc % kTDepth;                                                                   \
-        const uint32_t sa = stage_s + slot * kRowB + lofs;                                                    \
-        const uint32_t n0 = lds_u32(sa), n1 = lds_u32(sa + 4), n2 = lds_u32(sa + 8);                          \
-        const float4 wv = lds_f4(wrec_s + slot * 16);                                                         \
-        float2 fv[6];                                                                                         \
-        cvt_ring(n0, n1, n2, fv);                                                                             \
-        ++rc;                                                                                                 \
-        if ((slot & (kTGrp - 1)) == kTGrp - 1) group_done(slot / kTGrp, ((rc - 1) / kTDepth) & 1);             \
-        ring4<U>(acc, wv, fv);                                                                                \
-      }
-#define VP_V_RETIRE(U)                                                                                       \
-      {                                                                                                       \
-        const uint32_t rs = kStatic ? sbase + (uint32_t)U : rr % kNR;                                                 \
-        mbar_wait_uni<VP_TEAM_HINT>(&rempty[rs], ((rr / kNR) & 1) ^ 1);                                       \
-        const uint32_t so_ = rs * kSlotB;                                                                     \
-        const float4* a = acc[U];                     /* pixels 0..2 are quads .xyz; pixel 3 is the .w column */ \
-        sts_f4(vo[0] + so_, a[0]);                                                                            \
-        sts_f4(vo[1] + so_, a[1]);                                                                            \
-        sts_f4(vo[2] + so_, a[2]);                                                                            \
-        sts_f4(vo[3] + so_, make_float4(a[0].w, a[1].w, a[2].w, 0.f));                                        \
-        _Pragma("unroll") for (int q = 0; q < 3; ++q) acc[U][q] = make_float4(0.f, 0.f, 0.f, 0.f);            \
-        __syncwarp();                                                                                         \
-        mbar_arrive_if(&rfull[rs], l0 || VP_ALL_LANES_ARRIVE);                                                \
-        ++rr;                                                                                                 \
-      }
-      int4 ye_next = __ldg(reinterpret_cast<const int4*>(y1));
-      for (int ib = 0; ib < out_h; ib += 4) {
-        const int4 ye = ye_next;                  // window ends of rows ib..ib+3, prefetched one group ahead
-        const uint32_t sbase = kNR == 4 ? 0u : ((rr >> 2) % (uint32_t)(kNR / 4)) * 4u;   // retire slots of this group
-        if (ib + 4 < out_h) ye_next = __ldg(reinterpret_cast<const int4*>(y1 + ib + 4));
-#define VP_V_ROW(U, YE)                                                                                      \
-        if (kStatic || ib + U < out_h) {                                                                      \
-          const int yend = YE;                                                                                \
-          for (; y < yend; ++y) VP_V_BODY(U)                                                                  \
-          VP_V_RETIRE(U)                                                                                      \
+      } else {
+        // the group straddles items (or ends the CTA's range)
+#pragma unroll 1
+        for (int q = 0; q < kTGrp; ++q) {
+          if (y == in_h) {
+            if (++item >= my_b) { fin = true; break; }
+            open();
+          }
+          const uint32_t sa = gst + lofs + q * kRowB;
+          row(lds_u32(sa), lds_u32(sa + 4), lds_u32(sa + 8), lds_f4(gw + q * 16));
         }
-        VP_V_ROW(0, ye.x)
-        VP_V_ROW(1, ye.y)
-        VP_V_ROW(2, ye.z)
-        VP_V_ROW(3, ye.w)
-#undef VP_V_ROW
       }
-      // source rows below the last window (zero weights): keep the staging ring in step
-      for (; y < in_h; ++y) {
-        if ((rc & (kTGrp - 1)) == 0) mbar_wait_uni(&sfull[(rc / kTGrp) % kTNGrp], (rc / kTDepth) & 1);
-        const uint32_t slot = rc % kTDepth;
-        ++rc;
-        if ((slot & (kTGrp - 1)) == kTGrp - 1) group_done(slot / kTGrp, ((rc - 1) / kTDepth) & 1);
+      if (fin) break;
+      rc += kTGrp;
+      // the last V warp to finish group g refills it
+      if (VP_ALL_LANES_ARRIVE) mbar_arrive(&sread[g]);
+      __syncwarp();
+      int old = 0;
+      if (l0) {
+#ifdef VP_EXP_RELAT
+        asm volatile("atom.acq_rel.cta.shared::cta.add.u32 %0, [%1], 1;" : "=r"(old) : "r"(smem_u32(&gcnt[g])) : "memory");
+#else
+        __threadfence_block();
+        old = atomicAdd(&gcnt[g], 1);
+#endif
+        if (old == NV - 1) gcnt[g] = 0;
       }
-#undef VP_V_BODY
-#undef VP_V_RETIRE
+      if (__shfl_sync(0xffffffffu, old, 0) == NV - 1) {
+        if (VP_ALL_LANES_ARRIVE) mbar_wait_uni(&sread[g], par);
+        issue_group(g);
+      }
     }
     return;
   }
@@ -443,6 +522,9 @@ resize_split_kernel(FKParams kp, const vp_clip_plan* __restrict__ plans, const V
           wp[pp][tt] = kFold ? make_float2(wa * kp.scale[0], wb * kp.scale[0]) : make_float2(wa, wb);
           toff[pp][tt] = kLarge ? buf_s + (uint32_t)(xu - pa + u) * 16u        // padded row: base + 16 u
                                 : buf_s + (uint32_t)pos(min(x - pa, kPx - 1)) * 16u;   // slack taps (weight 0) stay in the row
+#ifdef VP_EXP_HBCAST
+          toff[pp][tt] = buf_s + (uint32_t)tt * 16u;
+#endif
         }
         const int jl0 = ja % B, wbk = ja / B, mw = jl0 / p, px = jl0 - mw * p;
         colpart[pp] = (wbk * m * m + mw) * D + px;
@@ -502,7 +584,9 @@ resize_split_kernel(FKParams kp, const vp_clip_plan* __restrict__ plans, const V
 #pragma unroll
           for (int pp = 0; pp < PPL; ++pp) qb[pp] = gb[pp] + U * p * kEsz;   // rows ib..ib+3 share i / p
           mbar_wait_uni<VP_TEAM_HINT>(&rfull[sbase + U], par);
+#ifndef VP_EXP_NOH
           hrow((sbase + (uint32_t)U) * kSlotB, qb);
+#endif
           __syncwarp();
           mbar_arrive_if(&rempty[sbase + U], l0 || VP_ALL_LANES_ARRIVE);
         }
@@ -551,7 +635,7 @@ team_vtab_kernel(const vp_clip_plan* __restrict__ plans, const int64_t* __restri
   if (!teamish(pl, coff[j], pitch[j]) || alias[j] != j) return;
   const int in_h = pl.in_h, out_h = pl.out_h;
   const int r = blockIdx.x * blockDim.x + threadIdx.x;
-  if (r < ((out_h + 3) & ~3)) y1tab[(int64_t)j * kTabOutH + r] = r < out_h ? window_of(in_h, out_h, r).x1 : in_h;
+  if (r < out_h + 4) y1tab[(int64_t)j * kTabOutStride + r] = r < out_h ? window_of(in_h, out_h, r).x1 : 0x7fffffff;
   if (r >= in_h) return;
   const int y = r;
   const double s = (double)in_h / (double)out_h;
@@ -566,7 +650,7 @@ team_vtab_kernel(const vp_clip_plan* __restrict__ plans, const int64_t* __restri
     if (w.x0 > y) break;
     const double sum = win_sum(w);
     const double wt = keys_d(((double)y - w.c + 0.5) * w.inv) / (sum != 0.0 ? sum : 1.0);
-    if (q < 4) wv[q] = (float)wt;
+    if (q < 4) wv[(i + q) & 3] = (float)wt;       // slot order: output row i + q lives in ring slot (i + q) % 4
     else if (fabs(wt) > 1e-9) atomicOr(&tflag[j], 1);     // a 5th live row with a non-negligible weight
   }
   vtab[(int64_t)j * kTabInH + y] = make_float4(wv[0], wv[1], wv[2], wv[3]);
@@ -725,7 +809,7 @@ ResizeWs resize_ws_layout(int n, void* base) {
   const size_t o_alias = take((size_t)n * sizeof(int));
   const size_t o_flag = take((size_t)n * sizeof(int));
   const size_t o_vtab = take((size_t)n * kTabInH * sizeof(float4));
-  const size_t o_y1 = take((size_t)n * kTabOutH * sizeof(int));
+  const size_t o_y1 = take((size_t)n * kTabOutStride * sizeof(int));
   const size_t o_u8 = take((size_t)n * sizeof(int2));
   w.bytes = o;
   char* b = reinterpret_cast<char*>(base);
@@ -774,7 +858,7 @@ void launch_split(const FKParams& kp, bool preset, const vp_clip_plan* plans, co
 cudaError_t launch_team(const FKParams& kp, const vp_clip_plan* plans, int n, const ResizeWs& w, const uint8_t* frames,
                         const int64_t* coff, const int64_t* pitch, void* pi, int64_t icap, void* pvv, int64_t vcap,
                         int32_t* clip_status, int dev, int num_sms, unsigned mask, cudaStream_t s) {
-  dim3 tg((kTabInH + 127) / 128, n);
+  dim3 tg((kTabInH + 127) / 128, n);   // kTabInH >= kTabOutStride
   team_vtab_kernel<<<tg, 128, 0, s>>>(plans, coff, pitch, w.alias, w.vtab, w.y1tab, w.tflag);
   const bool preset = kp.p == 16 && kp.m == 2 && kp.tp == 2;
   const bool team = (mask >> KV_TEAM) & 1u, wide = (mask >> KV_WIDE) & 1u, large = (mask >> KV_TEAML) & 1u;
