@@ -146,6 +146,19 @@ __host__ __device__ __forceinline__ TeamGeo team_geometry(int in_w, int out_w, i
   g.nslices = (out_w + ws - 1) / ws;
   return g;
 }
+// Row bands (KV_TEAM / KV_WIDE / KV_TEAML launches with too few items to fill the GPU, e.g. one clip): each frame's
+// output rows are cut into bands of a multiple of 4 rows (the H retire grouping), one work item per band; a band
+// reads the source rows of its windows (a few halo rows shared with its neighbours).  nb = bands per frame, chosen
+// per launch by variant_index_kernel (1 for large launches).
+constexpr int kMaxBands = 8;
+__host__ __device__ __forceinline__ int band_rows(int out_h, int nb) {
+  const int bs = (out_h + nb - 1) / nb;
+  return (bs + 3) & ~3;
+}
+__host__ __device__ __forceinline__ int band_count(int out_h, int nb) {
+  const int bs = band_rows(out_h, nb);
+  return (out_h + bs - 1) / bs;
+}
 __host__ __device__ __forceinline__ int variant_nv(int kv) { return kv == KV_WIDE ? kWideNV : kTeamNV; }
 __host__ __device__ __forceinline__ int variant_nh(int kv) { return kv == KV_WIDE ? kWideNH * kWidePPL : kTeamNH * kTeamPPL; }
 // taps of the union of two adjacent columns' windows: x1(j+1) - x0(j) < s + 4*fs + 1

@@ -184,7 +184,7 @@ struct ResizeWs {
   size_t bytes;
   int* list;          // [kNSlots][n]
   int64_t* off;       // [kNSlots][n+1]
-  int64_t* meta;      // [kNSlots][2]
+  int64_t* meta;      // [kNSlots][4]: clips, items, row bands per frame (team slots), unused
   int* alias;         // [n]  clip -> first clip of its run of equal (in_h, out_h) TEAM / WIDE clips (table owner)
   int* tflag;         // [n]  table flags (a non-negligible 5th live row)
   float4* vtab;       // [n][kTabInH]
@@ -195,7 +195,7 @@ ResizeWs resize_ws_layout(int n, void* base);
 VIdx ws_vidx(const ResizeWs& w, int n, int slot);
 int device_sms(int dev);
 cudaError_t launch_index(const vp_clip_plan* plans, int n, const int64_t* coff, const int64_t* pitch,
-                         const ResizeWs& w, cudaStream_t s);
+                         const ResizeWs& w, int num_sms, cudaStream_t s);
 cudaError_t launch_team(const FKParams& kp, const vp_clip_plan* plans, int n, const ResizeWs& w, const uint8_t* frames,
                         const int64_t* coff, const int64_t* pitch, void* pi, int64_t icap, void* pvv, int64_t vcap,
                         int32_t* clip_status, int dev, int num_sms, unsigned mask, cudaStream_t s);

@@ -418,7 +418,7 @@ extern "C" vp_status vp_resize_normalize_patchify(const vp_params* p, const vp_c
                         has(vp::KV_TEAM) || has(vp::KV_WIDE) || has(vp::KV_TEAML);
   if ((fast_aligned && any_fast) || has(vp::KV_U8)) {
     const vp::FKParams fk = vp::make_fkparams(p);
-    cudaError_t e = vp::launch_index(plans, n, clip_byte_offset, row_pitch, ws, s);
+    cudaError_t e = vp::launch_index(plans, n, clip_byte_offset, row_pitch, ws, sms, s);
     if (e == cudaSuccess && fast_aligned && (has(vp::KV_TEAM) || has(vp::KV_WIDE) || has(vp::KV_TEAML)))
       e = vp::launch_team(fk, plans, n, ws, frames, clip_byte_offset, row_pitch, pixel_values_images, img_rows_cap,
                           pixel_values_videos, vid_rows_cap, clip_status, dev, sms, mask, s);

@@ -8,24 +8,22 @@
 //      each staged source row once (I2F.U8 on the XU pipe for 2 of 3 words, PRMT + FADD2 for the third: both exact)
 //      and FMAs them (FFMA2, broadcast weight) into a 4-slot register ring of live output rows.  For a downscale
 //      (in >= out) at most 4 output rows are live at any source row (window 4s wide, centres s apart),
-//      so 4 slots carry no dead FMAs at the bench ratio.  Output row i lives in slot i % 4; the output-row loop is
-//      unrolled by 4 so every slot index is static.  A finished row is stored (float4 RGB + pad per pixel,
-//      sub-pixel-major swizzle: conflict-free stores, ~1.3x wavefronts for the H taps) into one of kNR retire
-//      slots: wait until the H warps released the slot (mbarrier rempty), store, arrive on rfull.
-//   H warps: lane (warp h, lane l) owns output column pair q = 32h + l of the slice; the pair's union window
-//      (<= kUL taps; weights (w_a, w_b) and the taps' shared addresses in registers for the whole slice) is read once
-//      per row (LDS.128) and FMA'd as 3 FFMA2 (pixel channel broadcast x pair weights); normalise (FFMA2), clamp in
-//      the output domain, pack bf16x2 / float2 and store straight into the HF patch layout, once per temporal slot
-//      the frame fills (O7); then release the retire slot.
-// The roles keep their own registers (V: the 48-register ring; H: 30 registers of slice state), so a CTA of 21
-// warps fits one SM with no spills, and V runs up to kNR rows ahead of H.
+//      so 4 slots carry no dead FMAs at the bench ratio.  Output row i lives in ring slot i % 4 and each source
+//      row's weight record is stored in slot order, so the FMAs of every row use static slots; the rows of a staging
+//      group are walked in pairs with the next row's loads issued ahead.  A finished row (switch on i % 4) is stored
+//      (float4 RGB + pad per pixel, conflict-free layout rpos) into one of kNR retire slots: wait until the H warps
+//      released the slot (mbarrier rempty), store, arrive on rfull.
+//   H warps: lane (warp h, lane l) owns output column pairs q = 32h + l (+ 32 NH per further pair) of the slice; the
+//      pair's union window (<= kUL taps; weights (w_a, w_b) and the taps' shared addresses in registers for the whole
+//      slice) is read once per row (LDS.128) and FMA'd as 3 FFMA2 (pixel channel broadcast x pair weights);
+//      normalise, clamp in the output domain, pack bf16x2 / float2 and store straight into the HF patch layout, once
+//      per temporal slot the frame fills (O7); then release the retire slot.
 //
-// Staging: each V warp keeps kTDepth source rows of its part in flight with cp.async.bulk (refilled in groups of
-// kTGrp rows, one mbarrier per group, producer state warp-uniform with the copies predicated to lane 0).  The
-// vertical weights travel with the rows: per source row a 16-B record (the fp32 weights of its <= 4 live output
-// rows, relative to the row being completed) copied by TMA from the per-clip table that team_vtab_kernel writes
-// into the caller's workspace (f64 Keys / f64 window sum -> fp32, C10).  Consecutive clips of equal (in_h, out_h)
-// share one table.
+// Staging: the CTA's source rows land in a kTDepth-row shared ring by cp.async.bulk, refilled in groups of kTGrp rows
+// (one mbarrier per group) by the last V warp to finish a group.  The vertical weights travel with the rows: per
+// source row a 16-B record (the fp32 weights of its <= 4 live output rows, in ring-slot order) copied by TMA from the
+// per-clip table that team_vtab_kernel writes into the caller's workspace (f64 Keys / f64 window sum -> fp32, C10).
+// Consecutive clips of equal (in_h, out_h) share one table.
 #include "vp_k3_common.cuh"
 #include <atomic>
 #include <type_traits>
@@ -89,9 +87,10 @@ struct TItem {
   int k;                    // clip index
   int s, f;                 // slice, frame
   int ws;                   // slice width
+  int r0, r1;               // output rows of the item's band [r0, r1) (the whole frame unless the launch is banded)
 };
 
-template <int NV, int NH>
+template <int NV, int NH, bool kBand>
 __device__ __forceinline__ TItem decode_item(const VIdx& vx, int cnt, int64_t item, const vp_clip_plan* plans, int p) {
   TItem t;
   t.j = vfind(vx, cnt, item);
@@ -99,9 +98,28 @@ __device__ __forceinline__ TItem decode_item(const VIdx& vx, int cnt, int64_t it
   const vp_clip_plan& pl = plans[t.k];
   t.ws = team_geometry(pl.in_w, pl.out_w, p, NV, NH).ws;
   const int64_t local = item - vx.off[t.j];
-  t.s = (int)(local / pl.n_frames);            // slice-major: consecutive items share the slice's H weights
-  t.f = (int)(local - (int64_t)t.s * pl.n_frames);
+  if (!kBand) {
+    t.s = (int)(local / pl.n_frames);          // slice-major: consecutive items share the slice's H weights
+    t.f = (int)(local - (int64_t)t.s * pl.n_frames);
+    t.r0 = 0;
+    t.r1 = pl.out_h;
+    return t;
+  }
+  const int nb = (int)vx.meta[2];
+  const int nbd = band_count(pl.out_h, nb), bs = band_rows(pl.out_h, nb);
+  const int64_t per_slice = (int64_t)pl.n_frames * nbd;
+  t.s = (int)(local / per_slice);
+  const int rem = (int)(local - (int64_t)t.s * per_slice);
+  const int b = rem / pl.n_frames;
+  t.f = rem - b * pl.n_frames;
+  t.r0 = b * bs;
+  t.r1 = min(pl.out_h, t.r0 + bs);
   return t;
+}
+
+// Source rows [ys, ye) of a band: from the first row of output row r0's window to the end of row r1-1's window.
+__device__ __forceinline__ int band_ys(const vp_clip_plan& pl, int r0) {
+  return r0 == 0 ? 0 : window_of(pl.in_h, pl.out_h, r0).x0;
 }
 
 // Slice span: output columns [j0, j0+jn), footprint pixels [pa, pa+np) with pa a multiple of 4.
@@ -133,28 +151,12 @@ __device__ __forceinline__ float byte_magic(uint32_t w, int k) {      // 2^23 + 
 }
 __device__ __forceinline__ void cvt_ring(uint32_t n0, uint32_t n1, uint32_t n2, float2 (&f)[6]) {
   const float2 mm = make_float2(-8388608.f, -8388608.f);
-#if defined(VP_EXP_NOI2F)
-  f[0] = __fadd2_rn(make_float2(byte_magic(n0, 0), byte_magic(n0, 1)), mm);
-  f[1] = __fadd2_rn(make_float2(byte_magic(n0, 2), byte_magic(n2, 1)), mm);
-  f[2] = __fadd2_rn(make_float2(byte_magic(n0, 3), byte_magic(n1, 0)), mm);
-  f[3] = __fadd2_rn(make_float2(byte_magic(n1, 1), byte_magic(n2, 2)), mm);
-  f[4] = __fadd2_rn(make_float2(byte_magic(n1, 2), byte_magic(n1, 3)), mm);
-  f[5] = __fadd2_rn(make_float2(byte_magic(n2, 0), byte_magic(n2, 3)), mm);
-#elif defined(VP_EXP_ALLI2F)
-  f[0] = make_float2(byte_i2f(n0, 0), byte_i2f(n0, 1));
-  f[1] = make_float2(byte_i2f(n0, 2), byte_i2f(n2, 1));
-  f[2] = make_float2(byte_i2f(n0, 3), byte_i2f(n1, 0));
-  f[3] = make_float2(byte_i2f(n1, 1), byte_i2f(n2, 2));
-  f[4] = make_float2(byte_i2f(n1, 2), byte_i2f(n1, 3));
-  f[5] = make_float2(byte_i2f(n2, 0), byte_i2f(n2, 3));
-#else
   f[0] = make_float2(byte_i2f(n0, 0), byte_i2f(n0, 1));                                   // R0 G0
   f[1] = __fadd2_rn(make_float2(byte_magic(n0, 2), byte_magic(n2, 1)), mm);               // B0 R3
   f[2] = make_float2(byte_i2f(n0, 3), byte_i2f(n1, 0));                                   // R1 G1
   f[3] = __fadd2_rn(make_float2(byte_magic(n1, 1), byte_magic(n2, 2)), mm);               // B1 G3
   f[4] = make_float2(byte_i2f(n1, 2), byte_i2f(n1, 3));                                   // R2 G2
   f[5] = make_float2(byte_i2f(n2, 0), byte_i2f(n2, 3));                                   // B2 B3
-#endif
 }
 
 // normalise (O6) as FFMA2 over the column pair, clamp (C12) in the output domain (clamp(v,0,255)*s+b ==
@@ -187,9 +189,6 @@ __device__ __forceinline__ void store_pair(const FKParams& kp, char* q, float2 a
       else *reinterpret_cast<uint32_t*>(d + (int64_t)c * cstride * kEsz) = o[c].x;
     }
   };
-#ifdef VP_EXP_NOSTG
-  if (o[0].x == 0x7fc17fc1u)
-#endif
   put(q);
   if (nslots > 1) {                                // frame n-1 also fills the temporal pad slots (O7)
     for (int s2 = 1, ti = ti0; s2 < nslots; ++s2) {
@@ -199,7 +198,7 @@ __device__ __forceinline__ void store_pair(const FKParams& kp, char* q, float2 a
   }
 }
 
-template <int NV, int NH, int PPL, int kUL, bool kF32, bool kFold, int P, int M, int TP, int MINB, bool kLarge>
+template <int NV, int NH, int PPL, int kUL, bool kF32, bool kFold, int P, int M, int TP, int MINB, bool kLarge, bool kBand>
 __global__ void __launch_bounds__((NV + NH) * 32, MINB)
 resize_split_kernel(FKParams kp, const vp_clip_plan* __restrict__ plans, const VIdx vx, const int* __restrict__ tab_alias,
                     const int* __restrict__ tab_flag, const float4* __restrict__ vtab, const int* __restrict__ y1tab,
@@ -222,6 +221,9 @@ resize_split_kernel(FKParams kp, const vp_clip_plan* __restrict__ plans, const V
   const bool l0 = lane == 0;
   const int p = P > 0 ? P : kp.p, m = P > 0 ? M : kp.m, tp = P > 0 ? TP : kp.tp;
 
+  // kBand: the instantiation for launches cut into row bands (variant_index_kernel's meta[2] > 1); both are launched
+  // and the one that does not match exits here, so the whole-frame path carries no band bookkeeping
+  if ((vx.meta[2] > 1) != kBand) return;
   const int cnt = (int)vx.meta[0];
   const int64_t total = vx.meta[1];
   const int64_t my_a = total * blockIdx.x / gridDim.x;
@@ -243,16 +245,18 @@ resize_split_kernel(FKParams kp, const vp_clip_plan* __restrict__ plans, const V
   // ---- staging producer: refill group g with the next kTGrp source rows of the CTA's item sequence (warp-uniform
   //      caller; the copies and barrier operations are predicated to lane 0) ----
   auto open_item = [&](TeamProd& st) {
-    const TItem t = decode_item<NV, NH * PPL>(vx, cnt, st.next, plans, p);
+    const TItem t = decode_item<NV, NH * PPL, kBand>(vx, cnt, st.next, plans, p);
     const vp_clip_plan& pl = plans[t.k];
     int j0, jn, pa, np;
     slice_span(pl, t.ws, t.s, j0, jn, pa, np);
     const int b0 = 3 * pa, o = b0 & 15;
+    const int ys = kBand ? band_ys(pl, t.r0) : 0;
+    const int ye = kBand ? __ldg(y1tab + (int64_t)tab_alias[t.k] * kTabOutStride + t.r1 - 1) : pl.in_h;
     st.nbytes = (o + 3 * np + 15) & ~15;
     st.pitch = pitch_arr[t.k];
-    st.src = frames + clip_off[t.k] + (int64_t)t.f * pl.in_h * st.pitch + (b0 - o);
-    st.wr = vtab + (int64_t)tab_alias[t.k] * kTabInH;
-    st.rows = pl.in_h;
+    st.src = frames + clip_off[t.k] + ((int64_t)t.f * pl.in_h + ys) * st.pitch + (b0 - o);
+    st.wr = vtab + (int64_t)tab_alias[t.k] * kTabInH + ys;
+    st.rows = ye - ys;
     ++st.next;
   };
   auto issue_group = [&](uint32_t g) {
@@ -328,71 +332,94 @@ resize_split_kernel(FKParams kp, const vp_clip_plan* __restrict__ plans, const V
     uint32_t rc = 0;                              // staged rows consumed (a multiple of kTGrp at every group start)
     uint32_t rr = 0;                              // output rows retired (all items)
     int64_t item = my_a;
-    int in_h = 0, y = 0, i = 0, nend = 0, nnext = 0;
+    int ye = 0, y = 0, i = 0, r0 = 0, r1 = 0, nend = 0, nnext = 0;
     uint32_t lofs = 0;                            // byte offset of this lane's 12 bytes inside a staged row
     const int* y1 = nullptr;
-    auto open = [&]() {                           // item `item`: its window ends and footprint offset
-      const TItem t = decode_item<NV, NH * PPL>(vx, cnt, item, plans, p);
+    auto open = [&]() {                           // item `item`: its band's source rows, window ends, footprint
+      const TItem t = decode_item<NV, NH * PPL, kBand>(vx, cnt, item, plans, p);
       const vp_clip_plan& pl = plans[t.k];
-      in_h = pl.in_h;
       const int pa = window_of(pl.in_w, pl.out_w, t.s * t.ws).x0 & ~3;
       y1 = y1tab + (int64_t)tab_alias[t.k] * kTabOutStride;
       lofs = (uint32_t)(((3 * pa) & 15) + 384 * warp + 12 * lane);   // the footprint starts at (3*pa) & 15
-      y = 0;
-      i = 0;
-      nend = __ldg(y1);
-      nnext = __ldg(y1 + 1);
+      r0 = t.r0;
+      r1 = t.r1;
+      if (!kBand) {
+        y = 0;
+        ye = pl.in_h;
+        i = 0;
+        nend = __ldg(y1);
+        nnext = __ldg(y1 + 1);
+        return;
+      }
+      y = band_ys(pl, r0);
+      ye = __ldg(y1 + r1 - 1);
+      // rows above the band still live at its first source row are accumulated and dropped (never stored): the
+      // ring slot of row r0-q is that of row r0+4-q, which starts only after row r0-q ended (<= 4 live rows)
+      i = r0;
+      while (i > 0 && __ldg(y1 + i - 1) > y) --i;
+      nend = __ldg(y1 + i);
+      nnext = __ldg(y1 + i + 1);
+      const float2 z2 = make_float2(0.f, 0.f);   // band items leave partial rows below r1 in the ring
+#pragma unroll
+      for (int r = 0; r < 4; ++r)
+#pragma unroll
+        for (int q = 0; q < 3; ++q) {
+          h2(acc[r][q], 0) = __fmul2_rn(h2(acc[r][q], 0), z2);
+          h2(acc[r][q], 1) = __fmul2_rn(h2(acc[r][q], 1), z2);
+        }
     };
-    // retire output row i (ring slot C = i % 4) into retire slot rr % kNR.  Preset geometry (kStatic: every out_h is
-    // a multiple of 4, so rr % 4 == i % 4): the retire slot is C itself and its addresses are immediates.
-    auto retire = [&](float4 (&a)[3], auto cslot) {
-      constexpr int C = decltype(cslot)::value;
-      const uint32_t rs = kStatic ? (uint32_t)C : rr % kNR;
-      mbar_wait_uni<VP_TEAM_HINT>(&rempty[rs], ((rr / kNR) & 1) ^ 1);
-      const uint32_t so_ = rs * kSlotB;
-      sts_f4(vo[0] + so_, a[0]);                 // pixels 0..2 are quads .xyz; pixel 3 is the .w column
-      sts_f4(vo[1] + so_, a[1]);
-      sts_f4(vo[2] + so_, a[2]);
-      sts_f4(vo[3] + so_, make_float4(a[0].w, a[1].w, a[2].w, 0.f));
-      // clear the slot as a[q] * 0 (6 FMUL2; the accumulators are finite): ptxas materialises literal zeros here as
-      // 18 uniform-register moves
+    // clear a ring slot as a[q] * 0 (6 FMUL2; the accumulators are finite): ptxas materialises literal zeros here as
+    // 18 uniform-register moves
+    auto clear = [&](float4 (&a)[3]) {
       const float2 z2 = make_float2(0.f, 0.f);
 #pragma unroll
       for (int q = 0; q < 3; ++q) {
         h2(a[q], 0) = __fmul2_rn(h2(a[q], 0), z2);
         h2(a[q], 1) = __fmul2_rn(h2(a[q], 1), z2);
       }
-      __syncwarp();
-      mbar_arrive_if(&rfull[rs], l0 || VP_ALL_LANES_ARRIVE);
-      ++rr;
+    };
+    // retire output row i (ring slot C = i % 4) into retire slot rr % kNR.  Preset geometry (kStatic: every out_h is
+    // a multiple of 4, so rr % 4 == i % 4): the retire slot is C itself and its addresses are immediates.  A row
+    // above the item's band (keep = false) is only cleared.
+    auto retire = [&](float4 (&a)[3], auto cslot, bool keep) {
+      constexpr int C = decltype(cslot)::value;
+      const uint32_t rs = kStatic ? (uint32_t)C : rr % kNR;
+      if (keep) {
+        mbar_wait_uni<VP_TEAM_HINT>(&rempty[rs], ((rr / kNR) & 1) ^ 1);
+        const uint32_t so_ = rs * kSlotB;
+        sts_f4(vo[0] + so_, a[0]);               // pixels 0..2 are quads .xyz; pixel 3 is the .w column
+        sts_f4(vo[1] + so_, a[1]);
+        sts_f4(vo[2] + so_, a[2]);
+        sts_f4(vo[3] + so_, make_float4(a[0].w, a[1].w, a[2].w, 0.f));
+      }
+      clear(a);
+      if (keep) {
+        __syncwarp();
+        mbar_arrive_if(&rfull[rs], l0 || VP_ALL_LANES_ARRIVE);
+        ++rr;
+      }
     };
     // one staged row (converted): FMA into the ring (static slots), retire the output rows it completes
     auto fma_row = [&](const float2 (&fv)[6], const float4 wv) {
       const float ws[4] = {wv.x, wv.y, wv.z, wv.w};
-#ifndef VP_EXP_NOV
 #pragma unroll
       for (int s = 0; s < 4; ++s) {
         const float2 ww = make_float2(ws[s], ws[s]);
 #pragma unroll
         for (int c = 0; c < 6; ++c) h2(acc[s][c >> 1], c & 1) = __ffma2_rn(ww, fv[c], h2(acc[s][c >> 1], c & 1));
       }
-#else
-      h2(acc[0][0], 0) = __fadd2_rn(h2(acc[0][0], 0), __fadd2_rn(fv[0], fv[5]));   // keep the conversions alive
-      h2(acc[1][0], 0) = __fadd2_rn(h2(acc[1][0], 0), __fadd2_rn(fv[1], fv[4]));
-      h2(acc[2][0], 0) = __fadd2_rn(h2(acc[2][0], 0), __fadd2_rn(fv[2], fv[3]));
-      acc[3][0].x += ws[0] + ws[3];
-#endif
       ++y;
       while (y == nend) {                         // source row y-1 completed output row i (ring slot i % 4)
+        const bool keep = !kBand || i >= r0;
         switch (i & 3) {
-          case 0: retire(acc[0], std::integral_constant<int, 0>{}); break;
-          case 1: retire(acc[1], std::integral_constant<int, 1>{}); break;
-          case 2: retire(acc[2], std::integral_constant<int, 2>{}); break;
-          default: retire(acc[3], std::integral_constant<int, 3>{}); break;
+          case 0: retire(acc[0], std::integral_constant<int, 0>{}, keep); break;
+          case 1: retire(acc[1], std::integral_constant<int, 1>{}, keep); break;
+          case 2: retire(acc[2], std::integral_constant<int, 2>{}, keep); break;
+          default: retire(acc[3], std::integral_constant<int, 3>{}, keep); break;
         }
         ++i;
-        nend = nnext;
-        nnext = __ldg(y1 + i + 1);                // the sentinels past out_h end the chain
+        nend = !kBand || i < r1 ? nnext : 0x7fffffff;   // the band (or the sentinels past out_h) ends the chain
+        nnext = __ldg(y1 + i + 1);
       }
     };
     auto row = [&](uint32_t n0, uint32_t n1, uint32_t n2, float4 wv) {
@@ -402,7 +429,7 @@ resize_split_kernel(FKParams kp, const vp_clip_plan* __restrict__ plans, const V
     };
     open();
     for (;;) {
-      if (y == in_h) {                            // item done (all its output rows retired)
+      if (y == ye) {                              // item done (all its output rows retired)
         if (++item >= my_b) break;
         open();
       }
@@ -412,7 +439,7 @@ resize_split_kernel(FKParams kp, const vp_clip_plan* __restrict__ plans, const V
       const uint32_t gst = stage_s + g * (kTGrp * kRowB);
       const uint32_t gw = wrec_s + g * (kTGrp * 16);
       bool fin = false;
-      if (in_h - y >= kTGrp) {
+      if (ye - y >= kTGrp) {
         // the whole group belongs to this item: rows in pairs with two register sets, each row's bytes loaded one
         // row and converted half a row ahead of its FMAs (the conversions of row q+1 overlap the FMAs of row q in
         // one basic block); the look-ahead past the group wraps to its own consumed rows (no stray reads).
@@ -444,7 +471,7 @@ resize_split_kernel(FKParams kp, const vp_clip_plan* __restrict__ plans, const V
         // the group straddles items (or ends the CTA's range)
 #pragma unroll 1
         for (int q = 0; q < kTGrp; ++q) {
-          if (y == in_h) {
+          if (y == ye) {
             if (++item >= my_b) { fin = true; break; }
             open();
           }
@@ -459,12 +486,8 @@ resize_split_kernel(FKParams kp, const vp_clip_plan* __restrict__ plans, const V
       __syncwarp();
       int old = 0;
       if (l0) {
-#ifdef VP_EXP_RELAT
-        asm volatile("atom.acq_rel.cta.shared::cta.add.u32 %0, [%1], 1;" : "=r"(old) : "r"(smem_u32(&gcnt[g])) : "memory");
-#else
         __threadfence_block();
         old = atomicAdd(&gcnt[g], 1);
-#endif
         if (old == NV - 1) gcnt[g] = 0;
       }
       if (__shfl_sync(0xffffffffu, old, 0) == NV - 1) {
@@ -487,9 +510,8 @@ resize_split_kernel(FKParams kp, const vp_clip_plan* __restrict__ plans, const V
   bool hact[PPL];
   uint32_t rr = 0;
   for (int64_t item = my_a; item < my_b; ++item) {
-    const TItem t = decode_item<NV, NH * PPL>(vx, cnt, item, plans, p);
+    const TItem t = decode_item<NV, NH * PPL, kBand>(vx, cnt, item, plans, p);
     const vp_clip_plan& pl = plans[t.k];
-    const int out_h = pl.out_h;
     if (hw == 0 && l0 && tab_flag[tab_alias[t.k]] != 0 && clip_status != nullptr) clip_status[t.k] = VP_EUNSUPPORTED;
     if (t.j != cur_j || t.s != cur_s) {
       // ---- K2 for this slice: union window of each of my column pairs, f64 Keys / f64 sums -> fp32 ----
@@ -522,9 +544,6 @@ resize_split_kernel(FKParams kp, const vp_clip_plan* __restrict__ plans, const V
           wp[pp][tt] = kFold ? make_float2(wa * kp.scale[0], wb * kp.scale[0]) : make_float2(wa, wb);
           toff[pp][tt] = kLarge ? buf_s + (uint32_t)(xu - pa + u) * 16u        // padded row: base + 16 u
                                 : buf_s + (uint32_t)pos(min(x - pa, kPx - 1)) * 16u;   // slack taps (weight 0) stay in the row
-#ifdef VP_EXP_HBCAST
-          toff[pp][tt] = buf_s + (uint32_t)tt * 16u;
-#endif
         }
         const int jl0 = ja % B, wbk = ja / B, mw = jl0 / p, px = jl0 - mw * p;
         colpart[pp] = (wbk * m * m + mw) * D + px;
@@ -569,7 +588,7 @@ resize_split_kernel(FKParams kp, const vp_clip_plan* __restrict__ plans, const V
       }
     };
     if (kStatic) {
-      for (int ib = 0; ib < out_h; ib += 4) {
+      for (int ib = t.r0; ib < t.r1; ib += 4) {
         // row offset of output row i (O8): (i / (m p)) * hb_stride + ((i / p) % m) * m * D + (i % p) * p; the 4 rows
         // of a group share i / p
         const int ro_grp = (ib / B) * hb_stride + ((ib / p) % m) * m * D + (ib % p) * p;
@@ -584,16 +603,14 @@ resize_split_kernel(FKParams kp, const vp_clip_plan* __restrict__ plans, const V
 #pragma unroll
           for (int pp = 0; pp < PPL; ++pp) qb[pp] = gb[pp] + U * p * kEsz;   // rows ib..ib+3 share i / p
           mbar_wait_uni<VP_TEAM_HINT>(&rfull[sbase + U], par);
-#ifndef VP_EXP_NOH
           hrow((sbase + (uint32_t)U) * kSlotB, qb);
-#endif
           __syncwarp();
           mbar_arrive_if(&rempty[sbase + U], l0 || VP_ALL_LANES_ARRIVE);
         }
         rr += 4;
       }
     } else {
-      for (int i = 0; i < out_h; ++i) {
+      for (int i = t.r0; i < t.r1; ++i) {
         const uint32_t rs = rr % kNR;
         mbar_wait_uni<VP_TEAM_HINT>(&rfull[rs], (rr / kNR) & 1);
         char* qb[PPL];
@@ -611,9 +628,9 @@ resize_split_kernel(FKParams kp, const vp_clip_plan* __restrict__ plans, const V
 
 
 // ---------------------------------------------------------------- per-clip vertical tables (K2 for KV_TEAM)
-// y1tab[j][i] = end of output row i's window (padded with in_h to a multiple of 4); vtab[j][y] = fp32 weights
-// (f64 Keys / f64 window sum, C10) of the output rows i(y)..i(y)+3, i(y) = first output row with y1 > y: the row
-// the kernel is completing when it consumes source row y.  One table per run of equal (in_h, out_h) in the list.
+// y1tab[j][i] = end of output row i's window (then 4 sentinels 0x7fffffff); vtab[j][y] = fp32 weights
+// (f64 Keys / f64 window sum, C10) of the output rows i(y)..i(y)+3 in ring-slot order (row r at r % 4), i(y) = first
+// output row with y1 > y: the row the kernel is completing when it consumes source row y.  One table per run of equal (in_h, out_h) in the list.
 __device__ __forceinline__ double win_sum(const Win& w) {
   double s = 0.0;
   for (int x = w.x0; x < w.x1; ++x) s += keys_d(((double)x - w.c + 0.5) * w.inv);
@@ -669,7 +686,7 @@ __device__ __forceinline__ int variant_slot(int kv) {
 __global__ void __launch_bounds__(kIdxThreads)
 variant_index_kernel(const vp_clip_plan* __restrict__ plans, int n, const int64_t* __restrict__ coff,
                      const int64_t* __restrict__ pitch, int* __restrict__ list, int64_t* __restrict__ off,
-                     int64_t* __restrict__ meta, int* __restrict__ alias, int* __restrict__ tflag) {
+                     int64_t* __restrict__ meta, int* __restrict__ alias, int* __restrict__ tflag, int num_sms) {
   __shared__ int64_t wsum[kIdxThreads / 32][kNSlots];
   __shared__ int wcnt[kIdxThreads / 32][kNSlots];
   __shared__ int64_t c_items[kNSlots];
@@ -730,10 +747,82 @@ variant_index_kernel(const vp_clip_plan* __restrict__ plans, int n, const int64_
     if (tid < kNSlots) { c_items[tid] += tot_items[tid]; c_cnt[tid] += tot_cnt[tid]; }
     __syncthreads();
   }
+  if (tid < kNSlots) off[(size_t)tid * (n + 1) + c_cnt[tid]] = c_items[tid];
+  // ---- row bands for the team slots (TEAM, WIDE, TEAML) of launches with too few items to fill the GPU ----
+  __shared__ unsigned long long tb[3][kMaxBands];
+  __shared__ int s_nb[kNSlots];
+  if (tid < 3 * kMaxBands) tb[tid / kMaxBands][tid % kMaxBands] = 0ull;
+  if (tid < kNSlots) s_nb[tid] = 1;
+  __syncthreads();
+  for (int v = 4; v <= 6; ++v) {
+    const int cn = c_cnt[v];
+    for (int q = tid; q < cn; q += kIdxThreads) {
+      const vp_clip_plan& pl = plans[list[(size_t)v * n + q]];
+#pragma unroll 1
+      for (int nb = 1; nb <= kMaxBands; ++nb)
+        atomicAdd(&tb[v - 4][nb - 1], (unsigned long long)pl.tile_count * band_count(pl.out_h, nb));
+    }
+  }
+  __syncthreads();
+  if (tid < 3) {
+    // CTAs of the launch: KV_WIDE one per SM, KV_TEAM / KV_TEAML two; score = busy fraction of the last wave,
+    // discounted 3% per extra band (halo rows, per-item setup); large launches keep whole frames
+    const int v = 4 + tid;
+    const double G = (double)num_sms * (v == 5 ? 1 : 2);
+    int best = 1;
+    if ((double)tb[tid][0] < 4.0 * G && tb[tid][0] > 0) {
+      double bs = -1.0;
+      for (int nb = 1; nb <= kMaxBands; ++nb) {
+        const double per = (double)tb[tid][nb - 1] / G;
+        const double eff = per < 1.0 ? per : per / ceil(per);
+        const double sc = eff / (1.0 + 0.03 * (nb - 1));
+        if (sc > bs + 1e-9) { bs = sc; best = nb; }
+      }
+    }
+    s_nb[v] = best;
+  }
+  __syncthreads();
+  for (int v = 4; v <= 6; ++v) {
+    const int nb = s_nb[v];
+    if (nb == 1) continue;
+    // rebuild the slot's item prefix with tile_count x bands per clip (block scan over its list)
+    int64_t carry = 0;
+    const int cn = c_cnt[v];
+    for (int c0 = 0; c0 < cn; c0 += kIdxThreads) {
+      const int q = c0 + tid;
+      int64_t x = 0;
+      if (q < cn) {
+        const vp_clip_plan& pl = plans[list[(size_t)v * n + q]];
+        x = (int64_t)pl.tile_count * band_count(pl.out_h, nb);
+      }
+      int64_t inc = x;
+#pragma unroll
+      for (int o = 1; o < 32; o <<= 1) {
+        const int64_t t = __shfl_up_sync(0xffffffffu, inc, o);
+        if (lane >= o) inc += t;
+      }
+      if (lane == 31) wsum[warp][0] = inc;
+      __syncthreads();
+      int64_t pre = carry, tot = 0;
+      for (int w = 0; w < kIdxThreads / 32; ++w) {
+        if (w < warp) pre += wsum[w][0];
+        tot += wsum[w][0];
+      }
+      if (q < cn) off[(size_t)v * (n + 1) + q] = pre + inc - x;
+      __syncthreads();
+      carry += tot;
+    }
+    if (tid == 0) {
+      off[(size_t)v * (n + 1) + cn] = carry;
+      c_items[v] = carry;
+    }
+    __syncthreads();
+  }
   if (tid < kNSlots) {
-    off[(size_t)tid * (n + 1) + c_cnt[tid]] = c_items[tid];
-    meta[2 * tid] = c_cnt[tid];
-    meta[2 * tid + 1] = c_items[tid];
+    meta[4 * tid] = c_cnt[tid];
+    meta[4 * tid + 1] = c_items[tid];
+    meta[4 * tid + 2] = s_nb[tid];
+    meta[4 * tid + 3] = 0;
   }
   __syncthreads();
   // table aliases: inclusive max-scan of run starts over the clips
@@ -805,7 +894,7 @@ ResizeWs resize_ws_layout(int n, void* base) {
   };
   const size_t o_list = take((size_t)kNSlots * n * sizeof(int));
   const size_t o_off = take((size_t)kNSlots * (n + 1) * sizeof(int64_t));
-  const size_t o_meta = take(2 * kNSlots * sizeof(int64_t));
+  const size_t o_meta = take(4 * kNSlots * sizeof(int64_t));
   const size_t o_alias = take((size_t)n * sizeof(int));
   const size_t o_flag = take((size_t)n * sizeof(int));
   const size_t o_vtab = take((size_t)n * kTabInH * sizeof(float4));
@@ -827,12 +916,13 @@ ResizeWs resize_ws_layout(int n, void* base) {
 }
 
 VIdx ws_vidx(const ResizeWs& w, int n, int slot) {
-  return VIdx{w.list + (size_t)slot * n, w.off + (size_t)slot * (n + 1), w.meta + 2 * slot};
+  return VIdx{w.list + (size_t)slot * n, w.off + (size_t)slot * (n + 1), w.meta + 4 * slot};
 }
 
 cudaError_t launch_index(const vp_clip_plan* plans, int n, const int64_t* coff, const int64_t* pitch,
-                         const ResizeWs& w, cudaStream_t s) {
-  variant_index_kernel<<<1, kIdxThreads, 0, s>>>(plans, n, coff, pitch, w.list, w.off, w.meta, w.alias, w.tflag);
+                         const ResizeWs& w, int num_sms, cudaStream_t s) {
+  variant_index_kernel<<<1, kIdxThreads, 0, s>>>(plans, n, coff, pitch, w.list, w.off, w.meta, w.alias, w.tflag,
+                                                   num_sms);
   return cudaGetLastError();
 }
 
@@ -844,15 +934,23 @@ void launch_split(const FKParams& kp, bool preset, const vp_clip_plan* plans, co
   // Qwen2.5/3-VL geometry (p16 m2 tp2) with compile-time output addressing, else runtime parameters
   // a channel-uniform scale (e.g. Qwen mean = std = 0.5) folds into the horizontal weights (store_pair)
   const bool fold = kp.scale[0] == kp.scale[1] && kp.scale[1] == kp.scale[2];
-  auto kern = preset ? (fold ? resize_split_kernel<NV, NH, PPL, kUL, kF32, true, 16, 2, 2, MINB, kLarge>
-                             : resize_split_kernel<NV, NH, PPL, kUL, kF32, false, 16, 2, 2, MINB, kLarge>)
-                     : resize_split_kernel<NV, NH, PPL, kUL, kF32, false, 0, 0, 0, MINB, kLarge>;
-  set_smem_attr(kern, dev, (int)Cfg::SMEM);
-  int per_sm = 0;
-  cudaOccupancyMaxActiveBlocksPerMultiprocessor(&per_sm, kern, Cfg::kThreads, Cfg::SMEM);
-  if (per_sm < 1) per_sm = 1;
-  kern<<<num_sms * per_sm, Cfg::kThreads, Cfg::SMEM, s>>>(kp, plans, vx, w.alias, w.tflag, w.vtab, w.y1tab, frames,
-                                                          coff, pitch, pi, icap, pvv, vcap, clip_status);
+  auto pick = [&](auto band) {
+    constexpr bool B = decltype(band)::value;
+    return preset ? (fold ? resize_split_kernel<NV, NH, PPL, kUL, kF32, true, 16, 2, 2, MINB, kLarge, B>
+                          : resize_split_kernel<NV, NH, PPL, kUL, kF32, false, 16, 2, 2, MINB, kLarge, B>)
+                  : resize_split_kernel<NV, NH, PPL, kUL, kF32, false, 0, 0, 0, MINB, kLarge, B>;
+  };
+  // whole-frame and row-band instantiations: the device-side band choice (meta[2]) lets exactly one of them run
+  auto launch = [&](auto kern) {
+    set_smem_attr(kern, dev, (int)Cfg::SMEM);
+    int per_sm = 0;
+    cudaOccupancyMaxActiveBlocksPerMultiprocessor(&per_sm, kern, Cfg::kThreads, Cfg::SMEM);
+    if (per_sm < 1) per_sm = 1;
+    kern<<<num_sms * per_sm, Cfg::kThreads, Cfg::SMEM, s>>>(kp, plans, vx, w.alias, w.tflag, w.vtab, w.y1tab, frames,
+                                                            coff, pitch, pi, icap, pvv, vcap, clip_status);
+  };
+  launch(pick(std::false_type{}));
+  launch(pick(std::true_type{}));
 }
 
 cudaError_t launch_team(const FKParams& kp, const vp_clip_plan* plans, int n, const ResizeWs& w, const uint8_t* frames,

@@ -390,3 +390,31 @@ def test_team_large_downscales(dtype):
     pl2 = _aligned_compare(pre2, [I.clip(2, 1.0, 1200, 1920), I.clip(2, 1.0, 1080, 1920)])
     kv2 = pl2.plans_host["kernel_variant"][:2].tolist()
     assert kv2[0] == KV_TEAML and kv2[1] in (0, 1, 2), kv2      # <= 1088 source rows: the fast streaming kernel
+
+
+@pytest.mark.parametrize("patch,merge,tp", [(6, 1, 1), (16, 2, 2), (14, 2, 2)])
+def test_team_row_bands(patch, merge, tp):
+    """Launches too small to fill the GPU cut each frame into row bands (one item per band, halo source rows shared
+    with the neighbours, rows of the band above accumulated and dropped): a single 720p clip and a two-clip batch
+    (KV_WIDE), a wide clip (KV_TEAM slices x bands) and a 1440p clip (KV_TEAML); non-preset geometry (p = 6, m = 1:
+    output heights not a multiple of 4) takes the dynamic retire-slot path.  Every element vs the oracle, and the
+    banded single-clip call byte-identical to the same clip inside a large (unbanded) batch."""
+    import paper_2604_16893_b200 as vp
+    f = patch * merge
+    pre = vp.VisualPreprocessor(patch_size=patch, merge_size=merge, temporal_patch_size=tp, max_frames=4,
+                                video_max_pixels=f * f * 160, image_max_pixels=f * f * 160, out_dtype=1)
+    _aligned_compare(pre, [I.clip(4, 1.0, 720, 1280)])
+    _aligned_compare(pre, [I.clip(3, 1.0, 720, 1280), I.clip(2, 1.0, 500, 900)])
+    _aligned_compare(pre, [I.clip(2, 1.0, 600, 2000)])
+    _aligned_compare(pre, [I.clip(2, 1.0, 1440, 2560)])
+    # byte identity: the clip alone (banded) vs the same clip first in a 150-clip batch (600 items: whole frames)
+    one = [I.clip(4, 1.0, 720, 1280)]
+    many = one * 150
+    op = oracle_params(pre.params)
+    fr = host_frames(O.plan_batch(op, one)[0], "noise")
+    _, _, _, out1 = _gpu_run(pre, one, frames=fr, align16=True)
+    _, _, _, out2 = _gpu_run(pre, many, frames=fr * 150, align16=True)
+    rows = int(out1["pixel_values_videos"].shape[0])
+    assert rows > 0
+    assert torch.equal(out1["pixel_values_videos"][:rows].view(torch.int16),
+                       out2["pixel_values_videos"][:rows].view(torch.int16))
