@@ -341,10 +341,12 @@ def measure_side(name: str, dev, steps: int = 10, warmup: int = 3):
 def k3_launches(mask: int, n: int) -> int:
     """Kernels one vp_resize_normalize_patchify call launches for a plan whose kernel-variant mask is `mask`
     (mirrors the dispatch in vp_resize.cu): grids + generic always; the work index when any TMA variant is present;
-    the team tables when team/wide clips are; one launch per present TMA variant; the direct kernel if needed."""
+    the team tables when team/wide clips are; one launch per present TMA variant (two per team variant: the
+    whole-frame and the row-band instantiation, one of which exits at once); the direct kernel if needed."""
     has = lambda v: (mask >> v) & 1
     tma = [has(v) for v in (0, 1, 2, 4, 5, 6, 8)]       # mild, medium, strong, copy, team, wide, team-large
-    n_l = (2 + (1 if (any(tma) or has(9)) else 0) + sum(tma) + (1 if (has(5) or has(6) or has(8)) else 0) + has(7)
+    team = has(5) + has(6) + has(8)                      # team variants launch a whole-frame and a row-band instance
+    n_l = (2 + (1 if (any(tma) or has(9)) else 0) + sum(tma) + team + (1 if team else 0) + has(7)
            + 2 * has(9))                                 # + direct; + u8 precision and u8 tiles
     return n_l if n > 0 else 0
 

@@ -1,6 +1,7 @@
 """Small invocations of every kernel of libvp for compute-sanitizer (memcheck / racecheck / synccheck / initcheck):
 the cfg1 clip, a mixed batch that takes every K3 variant (copy, team, wide, fast mild/medium, generic, direct,
-unaligned pitch -> generic), f32 and bf16, K4 on the matching token sequences, and the H10 records/pack kernels."""
+unaligned pitch -> generic), f32 and bf16, small launches (row-band team items) and a 300-clip launch (whole-frame
+team items), K4 on the matching token sequences, and the H10 records/pack kernels."""
 import os
 import sys
 
@@ -58,6 +59,15 @@ for dtype in (0, 1):
     one(pre, mixed, pad=1)
     big = vp.VisualPreprocessor(image_max_pixels=1024, video_max_pixels=1024, max_frames=3, out_dtype=dtype)
     one(big, [I.image(2000, 3000), I.clip(3, 2.0, 1500, 2600)])
+# a launch large enough for whole-frame items (the row-band instantiation exits at once): 300 two-frame 720p clips
+# sharing one frame buffer
+wide = vp.VisualPreprocessor(max_frames=2, video_max_pixels=65536, out_dtype=1)
+wc = [I.clip(2, 1.0, 720, 1280)] * 300
+wpl = wide.plan(wc)
+fr = host_frames(O.plan_batch(oracle_params(wide.params), wc[:1])[0])[0]
+wbuf, woff, wpit = pack_frames([fr], [3 * 1280])
+wide.run(wpl, wbuf, torch.zeros(300, dtype=torch.int64, device="cuda"), wpit.repeat(300), strict=False)
+torch.cuda.synchronize()
 # the round-2 kernels: u8 HF drop-in resize + linspace sampling, dedup/views, NV12 intake, vision ids, presets
 u8 = vp.VisualPreprocessor(max_frames=4, video_max_pixels=20000, image_max_pixels=30000, resize_mode=vp.VP_RESIZE_U8,
                            sampling=vp.VP_SAMPLE_LINSPACE)
