@@ -756,11 +756,18 @@ variant_index_kernel(const vp_clip_plan* __restrict__ plans, int n, const int64_
   __syncthreads();
   for (int v = 4; v <= 6; ++v) {
     const int cn = c_cnt[v];
-    for (int q = tid; q < cn; q += kIdxThreads) {
-      const vp_clip_plan& pl = plans[list[(size_t)v * n + q]];
+    // only launches with fewer than 4 items per CTA are candidates (large launches skip the band sums)
+    if ((double)c_items[v] >= 4.0 * num_sms * (v == 5 ? 1 : 2)) continue;
+    for (int c0 = 0; c0 < cn; c0 += kIdxThreads) {
+      const int q = c0 + tid;
+      const vp_clip_plan* pl = q < cn ? &plans[list[(size_t)v * n + q]] : nullptr;
 #pragma unroll 1
-      for (int nb = 1; nb <= kMaxBands; ++nb)
-        atomicAdd(&tb[v - 4][nb - 1], (unsigned long long)pl.tile_count * band_count(pl.out_h, nb));
+      for (int nb = 1; nb <= kMaxBands; ++nb) {
+        unsigned long long x = pl ? (unsigned long long)pl->tile_count * band_count(pl->out_h, nb) : 0ull;
+#pragma unroll
+        for (int o = 16; o > 0; o >>= 1) x += __shfl_xor_sync(0xffffffffu, x, o);
+        if (lane == 0 && x) atomicAdd(&tb[v - 4][nb - 1], x);
+      }
     }
   }
   __syncthreads();
