@@ -58,7 +58,8 @@ struct SplitCfg {
   // tap of a pair window is base + 16 u (no per-tap address registers, no clamping)
   static constexpr int kPxPad = kLarge ? kPx + kTeamULL : kPx;
   static constexpr int kThreads = (NV + NH) * 32;
-  static constexpr int kRowB = (NV * 384 + 16 + 15) & ~15;                // staged row: footprint + alignment slack
+  // staged row: footprint + alignment slack (KV_WIDE's single slice starts at pixel 0: no slack)
+  static constexpr int kRowB = NV == kWideNV ? NV * 384 : (NV * 384 + 16 + 15) & ~15;
   static constexpr size_t OFF_STG = 0;
   static constexpr size_t OFF_WREC = OFF_STG + (size_t)kTDepth * kRowB;
   static constexpr size_t OFF_BUF = OFF_WREC + (size_t)kTDepth * 16;
@@ -264,10 +265,16 @@ resize_split_kernel(FKParams kp, const vp_clip_plan* __restrict__ plans, const V
     TeamProd st = *ps;
     if (st.rows >= kTGrp) {
       mbar_expect_tx_if(&sfull[g], (uint32_t)(kTGrp * st.nbytes + kTGrp * 16), l0);
+      if (st.pitch == st.nbytes) {
+        // the copied span of each row is the whole row pitch: the group's rows are one contiguous block, one bulk copy
+        // (rows land at stride pitch <= kRowB; the V warps address whole groups at that stride)
+        tma_bulk_g2s_if(stage + (size_t)(g * kTGrp) * kRowB, st.src, (uint32_t)(kTGrp * st.nbytes), &sfull[g], l0);
+      } else {
 #pragma unroll
-      for (int q = 0; q < kTGrp; ++q)
-        tma_bulk_g2s_if(stage + (size_t)(g * kTGrp + q) * kRowB, st.src + (int64_t)q * st.pitch, (uint32_t)st.nbytes,
-                        &sfull[g], l0);
+        for (int q = 0; q < kTGrp; ++q)
+          tma_bulk_g2s_if(stage + (size_t)(g * kTGrp + q) * kRowB, st.src + (int64_t)q * st.pitch, (uint32_t)st.nbytes,
+                          &sfull[g], l0);
+      }
       tma_bulk_g2s_if(wrec + g * kTGrp, st.wr, kTGrp * 16, &sfull[g], l0);
       st.src += (int64_t)kTGrp * st.pitch;
       st.wr += kTGrp;
@@ -334,13 +341,18 @@ resize_split_kernel(FKParams kp, const vp_clip_plan* __restrict__ plans, const V
     int64_t item = my_a;
     int ye = 0, y = 0, i = 0, r0 = 0, r1 = 0, nend = 0, nnext = 0;
     uint32_t lofs = 0;                            // byte offset of this lane's 12 bytes inside a staged row
+    uint32_t gstride = kRowB;                     // row stride of a whole staging group (pitch when one bulk copy)
     const int* y1 = nullptr;
     auto open = [&]() {                           // item `item`: its band's source rows, window ends, footprint
       const TItem t = decode_item<NV, NH * PPL, kBand>(vx, cnt, item, plans, p);
       const vp_clip_plan& pl = plans[t.k];
-      const int pa = window_of(pl.in_w, pl.out_w, t.s * t.ws).x0 & ~3;
+      int j0, jn, pa, np;
+      slice_span(pl, t.ws, t.s, j0, jn, pa, np);
       y1 = y1tab + (int64_t)tab_alias[t.k] * kTabOutStride;
-      lofs = (uint32_t)(((3 * pa) & 15) + 384 * warp + 12 * lane);   // the footprint starts at (3*pa) & 15
+      const int o = (3 * pa) & 15;
+      lofs = (uint32_t)(o + 384 * warp + 12 * lane);   // the footprint starts at (3*pa) & 15
+      const int64_t pit = pitch_arr[t.k];
+      gstride = pit == (int64_t)((o + 3 * np + 15) & ~15) ? (uint32_t)pit : (uint32_t)kRowB;   // as issue_group
       r0 = t.r0;
       r1 = t.r1;
       if (!kBand) {
@@ -428,10 +440,14 @@ resize_split_kernel(FKParams kp, const vp_clip_plan* __restrict__ plans, const V
       fma_row(fv, wv);
     };
     open();
+    // fresh: this group starts an item, so the producer filled it row by row (issue_group opens items inside its
+    // per-row path): walk it with the per-row addressing
+    bool fresh = true;
     for (;;) {
       if (y == ye) {                              // item done (all its output rows retired)
         if (++item >= my_b) break;
         open();
+        fresh = true;
       }
       const uint32_t g = (rc / kTGrp) % kTNGrp;
       const uint32_t par = (rc / kTDepth) & 1;
@@ -439,13 +455,13 @@ resize_split_kernel(FKParams kp, const vp_clip_plan* __restrict__ plans, const V
       const uint32_t gst = stage_s + g * (kTGrp * kRowB);
       const uint32_t gw = wrec_s + g * (kTGrp * 16);
       bool fin = false;
-      if (ye - y >= kTGrp) {
+      if (!fresh && ye - y >= kTGrp) {
         // the whole group belongs to this item: rows in pairs with two register sets, each row's bytes loaded one
         // row and converted half a row ahead of its FMAs (the conversions of row q+1 overlap the FMAs of row q in
         // one basic block); the look-ahead past the group wraps to its own consumed rows (no stray reads).
         const uint32_t sb = gst + lofs;
         auto ld3 = [&](int r, uint32_t& x0, uint32_t& x1, uint32_t& x2) {
-          const uint32_t sa = sb + (uint32_t)r * kRowB;
+          const uint32_t sa = sb + (uint32_t)r * gstride;
           x0 = lds_u32(sa); x1 = lds_u32(sa + 4); x2 = lds_u32(sa + 8);
         };
         uint32_t ra0, ra1, ra2, rb0, rb1, rb2;
@@ -480,6 +496,7 @@ resize_split_kernel(FKParams kp, const vp_clip_plan* __restrict__ plans, const V
         }
       }
       if (fin) break;
+      fresh = false;
       rc += kTGrp;
       // the last V warp to finish group g refills it
       if (VP_ALL_LANES_ARRIVE) mbar_arrive(&sread[g]);
