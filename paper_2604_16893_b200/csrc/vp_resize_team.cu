@@ -20,7 +20,9 @@
 //      per temporal slot the frame fills (O7); then release the retire slot.
 //
 // Staging: the CTA's source rows land in a kTDepth-row shared ring by cp.async.bulk, refilled in groups of kTGrp rows
-// (one mbarrier per group) by the last V warp to finish a group.  The vertical weights travel with the rows: per
+// (one mbarrier per group) by the last V warp to finish a group; when the copied span of a row is the whole row
+// pitch (KV_WIDE frames packed at their pitch, e.g. cfg5) a group that does not start an item is one contiguous bulk
+// copy, its rows at stride pitch.  The vertical weights travel with the rows: per
 // source row a 16-B record (the fp32 weights of its <= 4 live output rows, in ring-slot order) copied by TMA from the
 // per-clip table that team_vtab_kernel writes into the caller's workspace (f64 Keys / f64 window sum -> fp32, C10).
 // Consecutive clips of equal (in_h, out_h) share one table.
@@ -35,7 +37,10 @@ namespace {
 #define VP_TEAM_DEPTH 16
 #endif
 constexpr int kTDepth = VP_TEAM_DEPTH;      // staged source rows per V warp
-constexpr int kTGrp = 8;                    // rows per refill group (one mbarrier phase)
+#ifndef VP_TEAM_GRP
+#define VP_TEAM_GRP 8
+#endif
+constexpr int kTGrp = VP_TEAM_GRP;          // rows per refill group (one mbarrier phase)
 constexpr int kTNGrp = kTDepth / kTGrp;
 #ifndef VP_TEAM_NR
 #define VP_TEAM_NR 4
