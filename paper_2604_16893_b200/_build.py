@@ -29,13 +29,20 @@ def build(verbose: bool = False, force: bool = False) -> str:
         return LIB
     objdir = os.path.join(HERE, "build")
     os.makedirs(objdir, exist_ok=True)
-    objs = []
-    for s in SOURCES:
+    extra = os.environ.get("VP_EXTRA_NVCC_FLAGS", "").split()   # experiments only
+
+    def compile_one(s: str):
         o = os.path.join(objdir, s.replace(".cu", ".o"))
-        extra = os.environ.get("VP_EXTRA_NVCC_FLAGS", "").split()   # experiments only
         cmd = [nvcc(), *ARCH, "-O3", "-lineinfo", "-std=c++17", "-Xcompiler", "-fPIC", "-Xptxas", "-v",
                "--expt-relaxed-constexpr", *PER_FILE.get(s, []), *extra, "-c", os.path.join(CSRC, s), "-o", o]
-        r = subprocess.run(cmd, capture_output=True, text=True)
+        return s, o, subprocess.run(cmd, capture_output=True, text=True)
+
+    # the translation units are independent: compile them in parallel (the team kernels' file dominates)
+    from concurrent.futures import ThreadPoolExecutor
+    with ThreadPoolExecutor(max_workers=max(1, min(len(SOURCES), os.cpu_count() or 1))) as ex:
+        results = list(ex.map(compile_one, SOURCES))
+    objs = []
+    for s, o, r in results:
         if r.returncode != 0:
             raise RuntimeError(f"nvcc failed for {s}:\n{r.stderr}")
         if verbose:
